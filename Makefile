@@ -1,0 +1,44 @@
+# Builds the engine's shared library in-tree (it travels to the GPU box with
+# gpurun) and the oracle checkers.
+#   paper_2108_03076_b200/libcltk_b200.so  -- sm_100a kernels + C++ host + C-ABI
+NVCC     ?= /usr/local/cuda/bin/nvcc
+HOSTCXX  := /usr/bin/g++
+NLOHMANN ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
+PKG      := paper_2108_03076_b200
+SRC      := $(PKG)/csrc
+OBJ      := build/obj
+LIB      := $(PKG)/libcltk_b200.so
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+
+CXXFLAGS := -std=c++17 -O2 -fPIC -ffp-contract=off -Wall -Wno-unused-function \
+            -I$(NLOHMANN) -I/usr/local/cuda/include -Iinclude
+NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -ccbin $(HOSTCXX) \
+            -Xcompiler -fPIC -Xptxas -v -Iinclude
+
+HOST_SRCS := host_model compiler engine capi
+HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS)))
+CU_OBJS   := $(OBJ)/mc_engine.o
+HDRS      := $(wildcard $(SRC)/*.hpp $(SRC)/*.h) include/cltk_b200.h
+
+.PHONY: all lib oracle clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	$(HOSTCXX) $(CXXFLAGS) -c $< -o $@
+
+$(OBJ)/mc_engine.o: $(SRC)/mc_engine.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/mc_engine.ptxas.txt || (cat $(OBJ)/mc_engine.ptxas.txt; false)
+	@grep -E "Used|spill" $(OBJ)/mc_engine.ptxas.txt | head -40
+
+$(LIB): $(HOST_OBJS) $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -cudart static -o $@ $^
+
+oracle:
+	$(MAKE) -C oracle all
+
+clean:
+	rm -rf build $(LIB)

@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""Benchmark: Monte Carlo paths/s of the barrier reverse convertible
+(3 underlyings x 367 dates, contracts/brc.cl; BASELINE.json metric) on
+1..8 B200s, with the FP64 roofline fraction and the reference CPU pricer
+timed beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step = one full pricing pass (simulate + payoff + reduce) over
+paths_per_gpu * N paths of the BRC kernel (weak scaling), inputs (the compiled
+program) resident on the device.  N > 1 runs one process per GPU under
+torch.distributed (NCCL); the only data-path collective is the single
+all_reduce of the chunk partials.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.setrecursionlimit(100000)
+
+METRIC = "MC paths/sec at 1/2/4/8 B200 (barrier reverse convertible), % FP roofline"
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+# FP64 flops per path of the fused kernel, frozen from the ncu SASS op counters
+# (dadd + dmul + 2*dfma) of the first correct kernel (profiles/).
+F_PATH = {"brc": None, "worst_off": None, "call": None}
+
+WORKLOADS = {
+    "brc": ("brc", "three", "BRC 3 underlyings x 367 dates (contracts/brc.cl, SURVEY.md App. A)"),
+    "worst_off": ("worst-off", "three", "worst-off autocallable 3 x 5 dates (contracts/worst-off.cl)"),
+    "call": ("european-call", "call", "European call 1 x 1 date (proj/contracts/european-call.cl)"),
+}
+
+
+def load(workload: str):
+    kname, mname, desc = WORKLOADS[workload]
+    kern = open(os.path.join(GOLD, "kernels", kname + ".json")).read()
+    model = open(os.path.join(GOLD, "models", mname + ".json")).read()
+    return kern, model, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def cpu_reference(kern_json: str, model_json: str, paths: int, seed: int, threads: int):
+    """The reference's own CPU pricer (oracle/_ref: the unmodified reference
+    compiled from its sources) when present, else the C restatement."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+    kern, model = json.loads(kern_json), json.loads(model_json)
+    if O.ref_available():
+        ref, kind = O.Ref(), "reference"
+        t0 = time.perf_counter()
+        r = ref.price(kern, model, paths, seed, [0], threads=threads)
+    else:
+        ref, kind = O.Oracle(), "port"
+        t0 = time.perf_counter()
+        r = ref.price(kern, model, paths, seed, [0], threads=threads)
+    dt = time.perf_counter() - t0
+    return kind, dt, r[0]
+
+
+def run_reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    kern, model, desc = load(args.workload)
+    threads = os.cpu_count() or 1
+    sample = args.ref_paths
+    for _ in range(args.warmup):
+        cpu_reference(kern, model, sample, 42, threads)
+    times = []
+    res = None
+    for _ in range(args.steps):
+        kind, dt, res = cpu_reference(kern, model, sample, 42, threads)
+        times.append(dt)
+    t = sum(times) / len(times)
+    v = sample / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "paths/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "paths_per_step": sample, "seed": 42,
+                       "engine": "reference priceMC, std::thread over host cores"},
+            "cpu_baseline": {"value": v, "unit": "paths/s", "cores": threads, "kind": kind,
+                             "sample": f"{sample} paths of the same workload per step"},
+            "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "price": res["price"], "std_error": res["std_error"]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="brc", choices=sorted(WORKLOADS))
+    ap.add_argument("--paths-per-gpu", type=int, default=125_000_000)
+    ap.add_argument("--ref-paths", type=int, default=100_000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2108_03076_b200 as E
+    from paper_2108_03076_b200.distributed import DistributedPricer
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    kern_json, model_json, desc = load(args.workload)
+    kern = E.Kernel(kern_json)
+    paths = args.paths_per_gpu * world
+    seed = 42
+    pricer = DistributedPricer(kern, model_json, [0], device=local)
+    info = pricer.plan.info
+    dev = torch.device(f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # FP64 peak on this GPU (DFMA microbenchmark, burst)
+    peak_tflops, _ = E.fp64_peak(local, 8192)
+
+    for _ in range(args.warmup):
+        pricer.finalize(paths, seed, pricer.launch(paths, seed))
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    step_ms = []
+    kernel_ms = []
+    res = None
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, nc = pricer.plan.chunking(paths)
+        parts = pricer.partials(paths)
+        parts.zero_()
+        c0, c1 = nc * rank // world, nc * (rank + 1) // world
+        pricer.plan.launch(paths, seed, c0, c1, parts.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        if world > 1:
+            dist.all_reduce(parts, op=dist.ReduceOp.SUM)
+        res = pricer.finalize(paths, seed, parts)  # combine + read-back (synchronises)
+        e2.record(stream)
+        e2.synchronize()
+        step_ms.append(e0.elapsed_time(e2))
+        kernel_ms.append(e0.elapsed_time(e1))
+    barrier()
+    clk = clocks.stop()
+    t_step = sum(step_ms) / len(step_ms)
+    t_kern = sum(kernel_ms) / len(kernel_ms)
+    if world > 1:
+        tt = torch.tensor([t_step, t_kern], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_kern = float(tt[0]), float(tt[1])
+    value = paths / (t_step * 1e-3)
+
+    # end to end through the public API, host JSON in -> host results out
+    e2e_times = []
+    for _ in range(args.e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        if world > 1:
+            from paper_2108_03076_b200 import distributed as D
+            D.price(E.Kernel(kern_json), model_json, paths, seed)
+        else:
+            E.price(kern_json, model_json, paths, seed)
+        torch.cuda.synchronize(dev)
+        e2e_times.append(time.perf_counter() - t0)
+    t_e2e = sum(e2e_times) / max(1, len(e2e_times))
+    if world > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    L = pricer.plan.dump()
+    h2d = (len(L["ops"]) * 8 + len(L["steps"]) * 208 + (L["n_shared_const"] + L["n_inst_const"]) * 8
+           + len(L["outputs"]) * 8 + 16 + len(kern_json) * 0)
+    d2h = info["n_outputs"] * 24 + 8
+
+    # roofline: FP64 pipe (the kernel reads only constants; no HBM term)
+    fpath = F_PATH.get(args.workload)
+    per_gpu_paths = paths / world
+    if fpath:
+        achieved = per_gpu_paths * fpath / (t_kern * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved / peak_tflops, "traffic": None,
+                "peak_source": "measured DFMA microbenchmark (cltk_fp64_peak), this GPU, burst",
+                "f_path": fpath}
+    else:
+        roof = {"bound": "fp64", "achieved": None, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": None, "traffic": None,
+                "peak_source": "measured DFMA microbenchmark (cltk_fp64_peak), this GPU, burst",
+                "f_path": None, "note": "F_path not yet frozen from ncu"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        kind, dt, r = cpu_reference(kern_json, model_json, args.ref_paths, seed, threads)
+        cpu = {"value": args.ref_paths / dt, "unit": "paths/s", "cores": threads, "kind": kind,
+               "sample": f"{args.ref_paths} paths of the same workload, seed {seed}, "
+                         f"{dt:.2f} s on {threads} threads",
+               "price": r["price"], "std_error": r["std_error"]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": desc, "paths_per_gpu": args.paths_per_gpu,
+                           "paths_per_step": paths, "seed": seed, "rng": "philox2x64-10",
+                           "parallelism": f"paths sharded over {world} GPU(s), 1 all_reduce",
+                           "l2": "flushed between timed steps (256 MiB write); inputs are a "
+                                 f"{h2d} B compiled program",
+                           "kernel_ms": t_kern},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": paths / t_e2e, "unit": "paths/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h,
+                        "path": "paper_2108_03076_b200.price -> cltk_gpu_price (C-ABI), host "
+                                "kernel/model JSON in, host results out"},
+                "gpu_launches": 2, "clocks": clk,
+                "price": res[0]["price"], "std_error": res[0]["std_error"],
+                "plan": {k: info[k] for k in ("n_shared_ops", "n_thread", "dag_nodes")}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

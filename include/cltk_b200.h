@@ -1,0 +1,135 @@
+/* cltk_b200.h -- C ABI of the B200 Monte Carlo pricing engine.
+ *
+ * The drop-in boundary for the reference's pricing path (cltk,
+ * arXiv 2108.03076).  Plain pointers and sizes only; no exceptions cross it.
+ * Structured inputs use the reference's own wire formats:
+ *   kernel  -- kernelToJson        (proj/src/kernel.cpp:620-629)
+ *   model   -- the model JSON       (proj/README.md:85-94, modelFromJson
+ *                                    proj/src/pricing.cpp:20-43)
+ *   tenv    -- tenvToJson           (proj/src/json_io.cpp:305-317)
+ * Every entry point returns 0 on success or the reference's ErrorCode
+ * (proj/include/cltk/errors.hpp:10-16: 2 parse, 3 type, 4 unsupported,
+ * 5 eval); err (may be NULL) receives the reference's message.  Device
+ * failures return 4 with a "device: ..." message.
+ *
+ * Entry point                replaces (reference interface)
+ * -------------------------  -------------------------------------------------
+ * cltk_gpu_price             cltk::priceAcrossTime  proj/include/cltk/pricing.hpp:92-98
+ *                            (and priceMC :84-89 with n_days = 1); the pybind
+ *                            cltk.price            proj/python/bindings.cpp:103-126
+ * cltk_gpu_price_batch       repeated priceAcrossTime over literal instances of one
+ *                            template (one path set, like repeated calls with one seed)
+ * cltk_plan_*                the same computation split for multi-GPU sharding:
+ *                            runParallel's path chunks (proj/src/pricing.cpp:268-286)
+ *                            become deterministic chunks any GPU can price.
+ * cltk_black_scholes_call    cltk::blackScholesCall proj/include/cltk/pricing.hpp:62-63
+ * cltk_debug_*               test hooks: per-path outputs, RNG streams
+ *                            (CounterRng proj/include/cltk/pricing.hpp:43-56)
+ */
+#ifndef CLTK_B200_H
+#define CLTK_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* PriceResult (proj/include/cltk/pricing.hpp:65-71) */
+typedef struct {
+  double price;
+  double std_error;
+  uint64_t paths;
+  uint64_t seed;
+  uint64_t valuation_day;
+} cltk_price_result;
+
+typedef struct {
+  int code;           /* ErrorCode, 0 = ok */
+  char message[504];
+} cltk_error;
+
+typedef struct cltk_plan cltk_plan;
+
+typedef struct {
+  uint32_t n_assets, n_steps, n_thread, n_shared_const, n_inst_const;
+  uint32_t n_instances, n_days, n_outputs;
+  uint32_t n_shared_ops, n_inst_ops, has_err, block;
+  uint64_t kernel_nodes, dag_nodes;
+} cltk_plan_info;
+
+/* Chunk partial written by cltk_plan_launch: count, mean, sum of squared
+ * deviations, for each output (instance-major, then valuation day). */
+typedef struct {
+  double n, mean, m2;
+} cltk_partial_t;
+
+const char* cltk_version(void);
+
+/* priceAcrossTime: results[n_days].  `threads` is accepted and ignored (the
+ * reference guarantees identical results for any value).  device < 0: the
+ * current CUDA device. */
+int cltk_gpu_price(const char* kernel_json, const char* model_json, uint64_t paths,
+                   uint64_t seed, const uint64_t* days, size_t n_days, const char* tenv_json,
+                   unsigned threads, int device, cltk_price_result* results, cltk_error* err);
+
+/* Template batch: n_instances kernels of one shape (differing only in float
+ * literals).  results[n_instances * n_days], instance-major. */
+int cltk_gpu_price_batch(const char* const* kernel_jsons, size_t n_instances,
+                         const char* model_json, uint64_t paths, uint64_t seed,
+                         const uint64_t* days, size_t n_days, const char* tenv_json, int device,
+                         cltk_price_result* results, cltk_error* err);
+
+/* ---- plan API: compile once, launch chunk ranges, combine --------------- */
+int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const char* model_json,
+                     const uint64_t* days, size_t n_days, const char* tenv_json, int device,
+                     int rewrite, cltk_plan** plan, cltk_error* err);
+void cltk_plan_destroy(cltk_plan* plan);
+int cltk_plan_get_info(const cltk_plan* plan, cltk_plan_info* info);
+/* Deterministic chunking of [0, paths): depends only on paths and the
+ * plan's output count, so a chunk range priced on any GPU yields the same
+ * partials. */
+int cltk_plan_chunking(const cltk_plan* plan, uint64_t paths, uint64_t* chunk_paths,
+                       uint64_t* n_chunks);
+/* Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream):
+ * price chunks [c0, c1) into partials_dev[c][out] (device memory of
+ * n_chunks * n_outputs cltk_partial_t). */
+int cltk_plan_launch(cltk_plan* plan, uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1,
+                     void* partials_dev, void* stream, cltk_error* err);
+/* Fixed-order combine of partials_dev[0, n_chunks), synchronous read-back,
+ * device error check.  results[n_instances * n_days]. */
+int cltk_plan_finalize(cltk_plan* plan, uint64_t paths, uint64_t seed, const void* partials_dev,
+                       const uint64_t* days, size_t n_days, void* stream,
+                       cltk_price_result* results, cltk_error* err);
+/* Device error word (min over paths of path << 24 | site; ~0 = none): read
+ * it, and overwrite it (e.g. with the MIN over ranks) before finalize. */
+int cltk_plan_error_word(cltk_plan* plan, void* stream, uint64_t* word);
+int cltk_plan_set_error_word(cltk_plan* plan, void* stream, uint64_t word);
+/* Host-only: compile (no device needed) and return the program listing --
+ * the engine's analogue of emitKernelSource (proj/src/kernel.cpp:407). */
+int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
+                         const char* model_json, const uint64_t* days, size_t n_days,
+                         const char* tenv_json, int rewrite, char** json, cltk_error* err);
+/* Program listing (JSON, malloc'd; free with cltk_free). */
+int cltk_plan_dump(const cltk_plan* plan, char** json);
+void cltk_free(void* p);
+
+/* ---- test hooks (same device code as the pricing kernel) --------------- */
+/* Per-path outputs [npaths][n_outputs]; spots/normals [npaths][n_steps][n_assets]
+ * (any may be NULL).  Host buffers. */
+int cltk_debug_paths(cltk_plan* plan, uint64_t seed, uint64_t path0, uint64_t npaths,
+                     double* outputs, double* spots, double* normals, uint64_t* error_word,
+                     cltk_error* err);
+/* Philox bits / uniforms / normals of stream (seed, path), indices [i0, i0+n). */
+int cltk_debug_rng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
+                   uint64_t* bits, double* uniforms, double* normals, cltk_error* err);
+/* Measured DFMA throughput (TFLOP/s) over `iters` iterations. */
+int cltk_fp64_peak(int device, int iters, double* tflops, double* seconds, cltk_error* err);
+
+double cltk_black_scholes_call(double spot, double strike, double rate, double vol,
+                               double t_years);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

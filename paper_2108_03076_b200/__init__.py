@@ -1,0 +1,367 @@
+"""B200-native Monte Carlo pricing of compiled contract kernels.
+
+The Python face of the engine mirrors the reference's pybind module
+(``cltk``, proj/python/bindings.cpp) for the pricing path:
+
+================================  ==============================================
+reference (``cltk``)              here
+================================  ==============================================
+``price(kernel, model, paths=100000, seed=0, days=[0], tenv={}, threads=0)``
+                                  same signature and result dicts
+                                  (bindings.cpp:103-126)
+``black_scholes_call``            same (bindings.cpp:128-129)
+``Kernel.rows`` / ``.cols``       same (bindings.cpp:75-80)
+``ContractError`` /               same hierarchy (bindings.cpp:47-49); eval
+``ContractParseError`` /          errors raise ``ContractError`` with
+``ContractTypeError``             ``.code == 5``, as the reference's do
+================================  ==============================================
+
+Kernels are the reference's flattened payoffs in its own wire format
+(``kernelToJson``, proj/src/kernel.cpp:620); the contract front end
+(parse/compile/cutPayoff/reindex) stays the reference's.  Everything below
+runs through ``libcltk_b200.so`` (sm_100a kernels + C++ host); there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import sys
+from typing import Any, Iterable, Sequence
+
+from . import _native
+
+__all__ = [
+    "Kernel", "ContractError", "ContractParseError", "ContractTypeError",
+    "ContractUnsupportedError", "price", "price_batch", "black_scholes_call", "Plan",
+    "compile_listing", "debug_rng", "fp64_peak", "load_kernel", "version",
+]
+
+
+class ContractError(Exception):
+    """cltk::Error (proj/include/cltk/errors.hpp:20-30); ``code`` = ErrorCode."""
+
+    def __init__(self, message: str, code: int = 5):
+        super().__init__(message)
+        self.code = code
+
+
+class ContractParseError(ContractError):
+    pass
+
+
+class ContractTypeError(ContractError):
+    pass
+
+
+class ContractUnsupportedError(ContractError):
+    pass
+
+
+def _raise(code: int, err: _native.ErrorC) -> None:
+    if code == 0:
+        return
+    msg = err.message.decode(errors="replace")
+    cls = {2: ContractParseError, 3: ContractTypeError, 4: ContractUnsupportedError}.get(
+        code, ContractError)
+    raise cls(msg, code)
+
+
+def _deep(fn, *a):
+    old = sys.getrecursionlimit()
+    sys.setrecursionlimit(max(old, 200000))
+    try:
+        return fn(*a)
+    finally:
+        sys.setrecursionlimit(old)
+
+
+class Kernel:
+    """A flattened payoff kernel (cltk::Kernel, proj/include/cltk/kernel.hpp:71-79)
+    held in the reference's JSON wire format."""
+
+    def __init__(self, source: str | dict):
+        if isinstance(source, dict):
+            self._obj = source
+            self._json = _deep(json.dumps, source)
+        else:
+            self._json = source
+            self._obj = _deep(json.loads, source)
+
+    @classmethod
+    def from_file(cls, path: str) -> "Kernel":
+        with open(path) as f:
+            return cls(f.read())
+
+    @property
+    def json(self) -> str:
+        return self._json
+
+    @property
+    def obj(self) -> dict:
+        return self._obj
+
+    rows = property(lambda self: list(self._obj["rows"]))
+    cols = property(lambda self: list(self._obj["cols"]))
+    tvars = property(lambda self: list(self._obj["tvars"]))
+    parties = property(lambda self: list(self._obj["parties"]))
+    horizon = property(lambda self: int(self._obj["horizon"]))
+
+    def literals(self) -> list[float]:
+        """FloatLit values in postorder (the order the engine's literal pool uses)."""
+        out: list[float] = []
+
+        def walk(e):
+            stack = [(e, False)]
+            while stack:
+                node, done = stack.pop()
+                k = node["kind"]
+                if done or k not in ("if", "loopif", "unop", "binop"):
+                    if k == "float":
+                        out.append(float(node["value"]))
+                    continue
+                stack.append((node, True))
+                kids = ([node["cond"], node["then"], node["else"]] if k in ("if", "loopif")
+                        else [node["arg"]] if k == "unop" else [node["left"], node["right"]])
+                for c in reversed(kids):
+                    stack.append((c, False))
+        walk(self._obj["body"])
+        return out
+
+    def with_literals(self, mapping: dict[float, float]) -> "Kernel":
+        """A new instance of the same template with FloatLit values substituted
+        (``{old_value: new_value}``): the "templated contract batch" input."""
+
+        def sub(e):
+            stack = [e]
+            while stack:
+                node = stack.pop()
+                k = node["kind"]
+                if k == "float":
+                    v = float(node["value"])
+                    if v in mapping:
+                        node["value"] = float(mapping[v])
+                elif k in ("if", "loopif"):
+                    stack += [node["cond"], node["then"], node["else"]]
+                elif k == "unop":
+                    stack.append(node["arg"])
+                elif k == "binop":
+                    stack += [node["left"], node["right"]]
+        obj = _deep(json.loads, self._json)
+        sub(obj["body"])
+        return Kernel(obj)
+
+
+def load_kernel(path: str) -> Kernel:
+    return Kernel.from_file(path)
+
+
+def _kernel_json(k: Kernel | str | dict) -> bytes:
+    if isinstance(k, Kernel):
+        return k.json.encode()
+    if isinstance(k, dict):
+        return _deep(json.dumps, k).encode()
+    return k.encode()
+
+
+def _model_json(m: str | dict) -> bytes:
+    return (m if isinstance(m, str) else json.dumps(m)).encode()
+
+
+def _tenv_json(t: dict | None) -> bytes:
+    return json.dumps(t or {}).encode()
+
+
+def _days(days: Iterable[int]):
+    d = [int(x) for x in days]
+    return (C.c_uint64 * max(1, len(d)))(*d), len(d)
+
+
+def _results(arr, n: int) -> list[dict]:
+    return [dict(price=arr[i].price, std_error=arr[i].std_error, paths=arr[i].paths,
+                 seed=arr[i].seed, valuation_day=arr[i].valuation_day) for i in range(n)]
+
+
+def version() -> str:
+    return _native.lib().cltk_version().decode()
+
+
+def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, seed: int = 0,
+          days: Sequence[int] = (0,), tenv: dict | None = None, threads: int = 0,
+          device: int = -1) -> list[dict]:
+    """priceAcrossTime on the GPU (cltk.price, proj/python/bindings.cpp:103-126).
+
+    Returns one dict per valuation day: ``price``, ``std_error``, ``paths``,
+    ``seed``, ``valuation_day``.  ``threads`` is accepted for compatibility
+    (results never depend on it)."""
+    L = _native.lib()
+    d, nd = _days(days)
+    out = (_native.PriceResultC * max(1, nd))()
+    err = _native.ErrorC()
+    rc = L.cltk_gpu_price(_kernel_json(kernel), _model_json(model), int(paths), int(seed), d, nd,
+                          _tenv_json(tenv), int(threads), int(device), out, C.byref(err))
+    _raise(rc, err)
+    return _results(out, nd)
+
+
+def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths: int = 100000,
+                seed: int = 0, days: Sequence[int] = (0,), tenv: dict | None = None,
+                device: int = -1) -> list[list[dict]]:
+    """Price literal instances of one template on one shared path set (no
+    recompilation per instance): ``[instance][day]`` result dicts."""
+    L = _native.lib()
+    d, nd = _days(days)
+    n = len(kernels)
+    arr = (C.c_char_p * n)(*[_kernel_json(k) for k in kernels])
+    out = (_native.PriceResultC * max(1, n * nd))()
+    err = _native.ErrorC()
+    rc = L.cltk_gpu_price_batch(arr, n, _model_json(model), int(paths), int(seed), d, nd,
+                                _tenv_json(tenv), int(device), out, C.byref(err))
+    _raise(rc, err)
+    flat = _results(out, n * nd)
+    return [flat[i * nd:(i + 1) * nd] for i in range(n)]
+
+
+def black_scholes_call(spot: float, strike: float, rate: float, vol: float,
+                       expiry: float) -> float:
+    return _native.lib().cltk_black_scholes_call(spot, strike, rate, vol, expiry)
+
+
+def compile_listing(kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
+                    days: Sequence[int] = (0,), tenv: dict | None = None,
+                    rewrite: bool = True) -> dict:
+    """Host-only compile: the streaming device program as JSON (no GPU needed)."""
+    if not isinstance(kernels, (list, tuple)):
+        kernels = [kernels]
+    L = _native.lib()
+    d, nd = _days(days)
+    arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
+    out = C.c_void_p()
+    err = _native.ErrorC()
+    rc = L.cltk_compile_listing(arr, len(kernels), _model_json(model), d, nd, _tenv_json(tenv),
+                                int(rewrite), C.byref(out), C.byref(err))
+    _raise(rc, err)
+    s = C.cast(out, C.c_char_p).value.decode()
+    L.cltk_free(out)
+    return _deep(json.loads, s)
+
+
+class Plan:
+    """Compiled plan on one device: the building block of multi-GPU pricing
+    (see ``paper_2108_03076_b200.distributed``)."""
+
+    def __init__(self, kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
+                 days: Sequence[int] = (0,), tenv: dict | None = None, device: int = -1,
+                 rewrite: bool = True):
+        if not isinstance(kernels, (list, tuple)):
+            kernels = [kernels]
+        self._L = _native.lib()
+        self.days = [int(x) for x in days]
+        d, nd = _days(self.days)
+        arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
+        self._h = C.c_void_p()
+        err = _native.ErrorC()
+        rc = self._L.cltk_plan_create(arr, len(kernels), _model_json(model), d, nd,
+                                      _tenv_json(tenv), int(device), int(rewrite),
+                                      C.byref(self._h), C.byref(err))
+        _raise(rc, err)
+        info = _native.PlanInfoC()
+        self._L.cltk_plan_get_info(self._h, C.byref(info))
+        self.info = {n: getattr(info, n) for n, _ in _native.PlanInfoC._fields_}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.cltk_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def n_outputs(self) -> int:
+        return int(self.info["n_outputs"])
+
+    def chunking(self, paths: int) -> tuple[int, int]:
+        cp, nc = C.c_uint64(), C.c_uint64()
+        self._L.cltk_plan_chunking(self._h, int(paths), C.byref(cp), C.byref(nc))
+        return cp.value, nc.value
+
+    def launch(self, paths: int, seed: int, c0: int, c1: int, partials_ptr: int,
+               stream_ptr: int = 0) -> None:
+        err = _native.ErrorC()
+        rc = self._L.cltk_plan_launch(self._h, int(paths), int(seed), int(c0), int(c1),
+                                      C.c_void_p(partials_ptr), C.c_void_p(stream_ptr),
+                                      C.byref(err))
+        _raise(rc, err)
+
+    def finalize(self, paths: int, seed: int, partials_ptr: int, stream_ptr: int = 0) -> list[dict]:
+        d, nd = _days(self.days)
+        n = self.n_outputs
+        out = (_native.PriceResultC * max(1, n))()
+        err = _native.ErrorC()
+        rc = self._L.cltk_plan_finalize(self._h, int(paths), int(seed), C.c_void_p(partials_ptr),
+                                        d, nd, C.c_void_p(stream_ptr), out, C.byref(err))
+        _raise(rc, err)
+        return _results(out, n)
+
+    def error_word(self, stream_ptr: int = 0) -> int:
+        w = C.c_uint64()
+        self._L.cltk_plan_error_word(self._h, C.c_void_p(stream_ptr), C.byref(w))
+        return w.value
+
+    def set_error_word(self, word: int, stream_ptr: int = 0) -> None:
+        self._L.cltk_plan_set_error_word(self._h, C.c_void_p(stream_ptr), C.c_uint64(word))
+
+    def dump(self) -> dict:
+        out = C.c_void_p()
+        self._L.cltk_plan_dump(self._h, C.byref(out))
+        s = C.cast(out, C.c_char_p).value.decode()
+        self._L.cltk_free(out)
+        return json.loads(s)
+
+    def debug_paths(self, seed: int, path0: int, npaths: int, spots: bool = False,
+                    normals: bool = False):
+        """Per-path outputs [npaths][n_outputs] (and optionally the simulated
+        spots / normals [npaths][n_steps][n_assets]) from the same device code."""
+        import numpy as np
+        ns, na = int(self.info["n_steps"]), max(1, int(self.info["n_assets"]))
+        outs = np.zeros((npaths, self.n_outputs))
+        S = np.zeros((npaths, ns, na)) if spots else None
+        Z = np.zeros((npaths, ns, na)) if normals else None
+        w = C.c_uint64()
+        err = _native.ErrorC()
+        rc = self._L.cltk_debug_paths(self._h, int(seed), int(path0), int(npaths),
+                                      outs.ctypes.data, S.ctypes.data if S is not None else None,
+                                      Z.ctypes.data if Z is not None else None, C.byref(w),
+                                      C.byref(err))
+        _raise(rc, err)
+        return outs, S, Z, w.value
+
+
+def debug_rng(seed: int, path: int, i0: int, n: int, device: int = -1):
+    """Philox bits / uniforms / normals of CounterRng(seed, path) indices
+    [i0, i0+n), computed by the device code the pricing kernel uses."""
+    import numpy as np
+    bits = np.zeros(n, dtype=np.uint64)
+    uni = np.zeros(n)
+    nor = np.zeros(n)
+    err = _native.ErrorC()
+    rc = _native.lib().cltk_debug_rng(int(device), int(seed), int(path), int(i0), int(n),
+                                      bits.ctypes.data, uni.ctypes.data, nor.ctypes.data,
+                                      C.byref(err))
+    _raise(rc, err)
+    return bits, uni, nor
+
+
+def fp64_peak(device: int = -1, iters: int = 4096) -> tuple[float, float]:
+    """Measured DFMA throughput in TFLOP/s (and the seconds it took)."""
+    t, s = C.c_double(), C.c_double()
+    err = _native.ErrorC()
+    rc = _native.lib().cltk_fp64_peak(int(device), int(iters), C.byref(t), C.byref(s),
+                                      C.byref(err))
+    _raise(rc, err)
+    return t.value, s.value

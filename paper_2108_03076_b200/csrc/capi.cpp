@@ -1,0 +1,217 @@
+// extern "C" boundary (include/cltk_b200.h).  Converts exceptions to the
+// reference's ErrorCode + message; no exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+
+#include "../../include/cltk_b200.h"
+#include "cltk_b200.hpp"
+#include "compiler.hpp"
+#include "engine_launch.hpp"
+
+using namespace cltk::b200;
+
+struct cltk_plan {
+  std::unique_ptr<Plan> plan;
+  std::vector<std::unique_ptr<Kernel>> kernels;
+};
+
+namespace {
+
+void setErr(cltk_error* err, int code, const char* msg) {
+  if (!err) return;
+  err->code = code;
+  std::strncpy(err->message, msg, sizeof(err->message) - 1);
+  err->message[sizeof(err->message) - 1] = 0;
+}
+
+template <class F>
+int guarded(cltk_error* err, F&& fn) {
+  try {
+    fn();
+    setErr(err, 0, "");
+    return 0;
+  } catch (const Error& e) {
+    setErr(err, static_cast<int>(e.code()), e.what());
+    return static_cast<int>(e.code());
+  } catch (const std::bad_alloc&) {
+    setErr(err, 4, "out of host memory");
+    return 4;
+  } catch (const std::exception& e) {
+    setErr(err, 4, e.what());
+    return 4;
+  }
+}
+
+void toC(const std::vector<PriceResult>& r, cltk_price_result* out) {
+  for (std::size_t i = 0; i < r.size(); ++i) {
+    out[i].price = r[i].price;
+    out[i].std_error = r[i].stdError;
+    out[i].paths = r[i].paths;
+    out[i].seed = r[i].seed;
+    out[i].valuation_day = r[i].valuationDay;
+  }
+}
+
+TEnv tenvOf(const char* j) { return (j && *j) ? tenvFromJson(j) : TEnv{}; }
+
+}  // namespace
+
+extern "C" {
+
+const char* cltk_version(void) { return "cltk-b200 0.1 (sm_100a)"; }
+
+void cltk_free(void* p) { std::free(p); }
+
+double cltk_black_scholes_call(double spot, double strike, double rate, double vol, double t) {
+  return blackScholesCall(spot, strike, rate, vol, t);
+}
+
+int cltk_gpu_price(const char* kernel_json, const char* model_json, uint64_t paths, uint64_t seed,
+                   const uint64_t* days, size_t n_days, const char* tenv_json, unsigned threads,
+                   int device, cltk_price_result* results, cltk_error* err) {
+  return guarded(err, [&] {
+    if (paths == 0) throw EvalError("path count must be positive");
+    Kernel k = kernelFromJson(kernel_json);
+    ModelSpec m = modelFromJson(model_json);
+    std::vector<uint64_t> d(days, days + n_days);
+    RunOptions opt;
+    opt.device = device;
+    (void)threads;
+    auto r = priceBatch({&k}, m, paths, seed, d, tenvOf(tenv_json), opt);
+    toC(r, results);
+  });
+}
+
+int cltk_gpu_price_batch(const char* const* kernel_jsons, size_t n_instances,
+                         const char* model_json, uint64_t paths, uint64_t seed,
+                         const uint64_t* days, size_t n_days, const char* tenv_json, int device,
+                         cltk_price_result* results, cltk_error* err) {
+  return guarded(err, [&] {
+    if (paths == 0) throw EvalError("path count must be positive");
+    std::vector<Kernel> ks;
+    ks.reserve(n_instances);
+    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromJson(kernel_jsons[i]));
+    std::vector<const Kernel*> ptrs;
+    for (auto& k : ks) ptrs.push_back(&k);
+    ModelSpec m = modelFromJson(model_json);
+    std::vector<uint64_t> d(days, days + n_days);
+    RunOptions opt;
+    opt.device = device;
+    toC(priceBatch(ptrs, m, paths, seed, d, tenvOf(tenv_json), opt), results);
+  });
+}
+
+int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const char* model_json,
+                     const uint64_t* days, size_t n_days, const char* tenv_json, int device,
+                     int rewrite, cltk_plan** out, cltk_error* err) {
+  return guarded(err, [&] {
+    auto p = std::make_unique<cltk_plan>();
+    std::vector<const Kernel*> ptrs;
+    for (size_t i = 0; i < n_instances; ++i) {
+      p->kernels.push_back(std::make_unique<Kernel>(kernelFromJson(kernel_jsons[i])));
+      ptrs.push_back(p->kernels.back().get());
+    }
+    ModelSpec m = modelFromJson(model_json);
+    std::vector<uint64_t> d(days, days + n_days);
+    RunOptions opt;
+    opt.device = device;
+    opt.rewrite = rewrite != 0;
+    p->plan = std::make_unique<Plan>(ptrs, m, d, tenvOf(tenv_json), opt);
+    *out = p.release();
+  });
+}
+
+void cltk_plan_destroy(cltk_plan* plan) { delete plan; }
+
+int cltk_plan_get_info(const cltk_plan* plan, cltk_plan_info* info) {
+  PlanInfo i = plan->plan->info();
+  static_assert(sizeof(PlanInfo) == sizeof(cltk_plan_info), "info layout");
+  std::memcpy(info, &i, sizeof i);
+  return 0;
+}
+
+int cltk_plan_chunking(const cltk_plan* plan, uint64_t paths, uint64_t* chunk_paths,
+                       uint64_t* n_chunks) {
+  plan->plan->chunking(paths, chunk_paths, n_chunks);
+  return 0;
+}
+
+int cltk_plan_launch(cltk_plan* plan, uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1,
+                     void* partials_dev, void* stream, cltk_error* err) {
+  return guarded(err, [&] { plan->plan->launch(paths, seed, c0, c1, partials_dev, stream); });
+}
+
+int cltk_plan_finalize(cltk_plan* plan, uint64_t paths, uint64_t seed, const void* partials_dev,
+                       const uint64_t* days, size_t n_days, void* stream,
+                       cltk_price_result* results, cltk_error* err) {
+  return guarded(err, [&] {
+    auto r = plan->plan->finalize(paths, seed, partials_dev, stream);
+    if (n_days)
+      for (std::size_t i = 0; i < r.size(); ++i) r[i].valuationDay = days[i % n_days];
+    toC(r, results);
+  });
+}
+
+int cltk_plan_error_word(cltk_plan* plan, void* stream, uint64_t* word) {
+  cltk_error e;
+  return guarded(&e, [&] { *word = planErrorWord(*plan->plan, stream); });
+}
+
+int cltk_plan_set_error_word(cltk_plan* plan, void* stream, uint64_t word) {
+  cltk_error e;
+  return guarded(&e, [&] { planSetErrorWord(*plan->plan, stream, word); });
+}
+
+int cltk_debug_paths(cltk_plan* plan, uint64_t seed, uint64_t path0, uint64_t npaths,
+                     double* outputs, double* spots, double* normals, uint64_t* error_word,
+                     cltk_error* err) {
+  return guarded(err, [&] {
+    uint64_t w = debugPaths(*plan->plan, seed, path0, npaths, outputs, spots, normals);
+    if (error_word) *error_word = w;
+  });
+}
+
+int cltk_debug_rng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
+                   uint64_t* bits, double* uniforms, double* normals, cltk_error* err) {
+  return guarded(err, [&] { debugRng(device, seed, path, i0, n, bits, uniforms, normals); });
+}
+
+int cltk_fp64_peak(int device, int iters, double* tflops, double* seconds, cltk_error* err) {
+  return guarded(err, [&] { *tflops = fp64Peak(device, iters, seconds); });
+}
+
+int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
+                         const char* model_json, const uint64_t* days, size_t n_days,
+                         const char* tenv_json, int rewrite, char** json, cltk_error* err) {
+  return guarded(err, [&] {
+    std::vector<Kernel> ks;
+    ks.reserve(n_instances);
+    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromJson(kernel_jsons[i]));
+    std::vector<const Kernel*> ptrs;
+    for (auto& k : ks) ptrs.push_back(&k);
+    if (ptrs.empty()) throw EvalError("no kernel instances");
+    ModelSpec m = modelFromJson(model_json);
+    SimPlanHost sp = buildSimPlan(*ptrs[0], m);
+    TEnv t = tenvOf(tenv_json);
+    for (const auto& v : ptrs[0]->tvars) (void)t.lookup(v);
+    CompileOptions co;
+    co.rewrite = rewrite != 0;
+    CompiledProgram P = compileProgram(ptrs, sp, std::vector<uint64_t>(days, days + n_days), co);
+    char* p = static_cast<char*>(std::malloc(P.listing.size() + 1));
+    std::memcpy(p, P.listing.c_str(), P.listing.size() + 1);
+    *json = p;
+  });
+}
+
+int cltk_plan_dump(const cltk_plan* plan, char** json) {
+  std::string s = plan->plan->dump();
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  *json = p;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,387 @@
+// Host orchestration of the B200 engine: plan upload, deterministic chunking,
+// launches, fixed-order combine, error word -> reference exception.
+// The reference pricing functions (priceMC / priceAcrossTime,
+// proj/src/pricing.cpp:318-371) are re-implemented on top of it with the
+// same argument meaning and error behaviour.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "cltk_b200.hpp"
+#include "compiler.hpp"
+#include "engine_launch.hpp"
+
+namespace cltk {
+namespace b200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
+  if (v.empty()) return nullptr;
+  void* p = nullptr;
+  ck(cudaMalloc(&p, v.size() * sizeof(T)), "cudaMalloc");
+  ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+constexpr uint64_t kMaxChunks = 1ULL << 20;
+constexpr uint64_t kPartialBudget = 1ULL << 30;  // bytes of chunk partials
+
+}  // namespace
+
+struct PlanImpl {
+  CompiledProgram prog;
+  DevPlan dev{};
+  int device = 0;
+  int sms = 0;
+  std::vector<void*> owned;
+  unsigned long long* errKey = nullptr;
+  unsigned long long* chunkCounter = nullptr;
+  cltk_partial* combined = nullptr;  // [n_out]
+  double* accScratch = nullptr;
+  size_t accScratchBlocks = 0;
+  cltk_partial* ownPartials = nullptr;  // used by the one-shot entry points
+  uint64_t ownPartialsChunks = 0;
+  size_t smem = 0;
+  bool accInSmem = true;
+  int blocksPerSm = 0;
+  uint32_t nOut = 0;
+
+  ~PlanImpl() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    for (void* p : owned) cudaFree(p);
+    if (accScratch) cudaFree(accScratch);
+    if (ownPartials) cudaFree(ownPartials);
+    cudaSetDevice(cur);
+  }
+
+  struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int d) {
+      cudaGetDevice(&prev);
+      if (prev != d) ck(cudaSetDevice(d), "cudaSetDevice");
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+  };
+};
+
+Plan::Plan(const std::vector<const Kernel*>& instances, const ModelSpec& model,
+           const std::vector<uint64_t>& days, const TEnv& tenv, const RunOptions& opt)
+    : impl_(new PlanImpl) {
+  if (instances.empty()) throw EvalError("no kernel instances");
+  PlanImpl& I = *impl_;
+  // Reference order of checks: SimPlan ctor, then the tenv lookups
+  // (proj/src/pricing.cpp:335-338).
+  SimPlanHost sp = buildSimPlan(*instances[0], model);
+  for (const auto& v : instances[0]->tvars) (void)tenv.lookup(v);
+  CompileOptions co;
+  co.rewrite = opt.rewrite;
+  I.prog = compileProgram(instances, sp, days, co);
+  I.nOut = I.prog.header.n_instances * I.prog.header.n_days;
+
+  int dev = opt.device;
+  if (dev < 0) ck(cudaGetDevice(&dev), "cudaGetDevice");
+  I.device = dev;
+  PlanImpl::DeviceGuard g(dev);
+  ck(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+  I.dev.hdr = I.prog.header;
+  I.dev.steps = upload(I.prog.steps, I.owned);
+  I.dev.code = upload(I.prog.code, I.owned);
+  I.dev.sharedConst = upload(I.prog.sharedConst, I.owned);
+  I.dev.instConst = upload(I.prog.instConst, I.owned);
+  I.dev.outputs = upload(I.prog.outputs, I.owned);
+  void* p = nullptr;
+  ck(cudaMalloc(&p, 2 * sizeof(unsigned long long)), "cudaMalloc");
+  I.owned.push_back(p);
+  I.errKey = static_cast<unsigned long long*>(p);
+  I.chunkCounter = I.errKey + 1;
+  ck(cudaMemset(I.errKey, 0xff, sizeof(unsigned long long)), "cudaMemset");
+  ck(cudaMalloc(&p, std::max<size_t>(1, I.nOut) * sizeof(cltk_partial)), "cudaMalloc");
+  I.owned.push_back(p);
+  I.combined = static_cast<cltk_partial*>(p);
+  I.accInSmem = accFitsSmem(I.prog.header);
+  I.smem = pathKernelSmem(I.prog.header, I.accInSmem);
+  if (I.smem > 227 * 1024)
+    throw UnsupportedError("compiled payoff needs " + std::to_string(I.smem) +
+                           " bytes of shared memory per CTA (max 232448)");
+  I.blocksPerSm = pathKernelOccupancy(I.prog.header, I.smem);
+  if (I.blocksPerSm <= 0) throw DeviceError("path kernel cannot be resident");
+}
+
+Plan::~Plan() = default;
+
+PlanInfo Plan::info() const {
+  const PlanImpl& I = *impl_;
+  const cltk_plan_header& h = I.prog.header;
+  PlanInfo r{};
+  r.n_assets = h.n_assets;
+  r.n_steps = h.n_steps;
+  r.n_thread = h.n_thread;
+  r.n_shared_const = h.n_shared_const;
+  r.n_inst_const = h.n_inst_const;
+  r.n_instances = h.n_instances;
+  r.n_days = h.n_days;
+  r.n_outputs = I.nOut;
+  r.n_shared_ops = I.prog.nSharedOps;
+  r.n_inst_ops = I.prog.nInstOps;
+  r.has_err = h.has_err;
+  r.block = kBlock;
+  r.kernel_nodes = I.prog.kernelNodes;
+  r.dag_nodes = I.prog.dagNodes;
+  return r;
+}
+
+void Plan::chunking(uint64_t paths, uint64_t* chunkPaths, uint64_t* nChunks) const {
+  // A function of (paths, n_outputs) only -- never of the GPU count.
+  const uint64_t nOut = std::max<uint32_t>(1, impl_->nOut);
+  uint64_t maxChunks = std::min<uint64_t>(kMaxChunks, kPartialBudget / (sizeof(cltk_partial) * nOut));
+  maxChunks = std::max<uint64_t>(1, maxChunks);
+  uint64_t ppt = (paths + kBlock * maxChunks - 1) / (kBlock * maxChunks);
+  ppt = std::max<uint64_t>(1, ppt);
+  *chunkPaths = ppt * kBlock;
+  *nChunks = (paths + *chunkPaths - 1) / *chunkPaths;
+}
+
+void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void* partialsDev,
+                  void* stream) {
+  if (paths == 0) throw EvalError("path count must be positive");
+  PlanImpl& I = *impl_;
+  PlanImpl::DeviceGuard g(I.device);
+  uint64_t chunkPaths, nChunks;
+  chunking(paths, &chunkPaths, &nChunks);
+  c1 = std::min(c1, nChunks);
+  if (c0 >= c1) return;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t work = c1 - c0;
+  int grid = static_cast<int>(std::min<uint64_t>(work, static_cast<uint64_t>(I.sms) * I.blocksPerSm));
+  if (!I.accInSmem) {
+    size_t need = static_cast<size_t>(grid);
+    if (need > I.accScratchBlocks) {
+      if (I.accScratch) cudaFree(I.accScratch);
+      ck(cudaMalloc(&I.accScratch, need * kWarps * I.nOut * 3 * sizeof(double)), "cudaMalloc");
+      I.accScratchBlocks = need;
+    }
+  }
+  ck(cudaMemsetAsync(I.chunkCounter, 0, sizeof(unsigned long long), s), "cudaMemsetAsync");
+  RunArgs a{};
+  a.seed = seed;
+  a.paths = paths;
+  a.chunkPaths = chunkPaths;
+  a.ppt = static_cast<uint32_t>(chunkPaths / kBlock);
+  a.c0 = c0;
+  a.c1 = c1;
+  a.partials = static_cast<cltk_partial*>(partialsDev);
+  a.errKey = I.errKey;
+  a.chunkCounter = I.chunkCounter;
+  a.accScratch = I.accScratch;
+  ck(launchPath(I.dev, a, grid, I.smem, s), "path kernel launch");
+}
+
+std::vector<PriceResult> Plan::finalize(uint64_t paths, uint64_t seed, const void* partialsDev,
+                                        void* stream) {
+  if (paths == 0) throw EvalError("path count must be positive");
+  PlanImpl& I = *impl_;
+  PlanImpl::DeviceGuard g(I.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint64_t chunkPaths, nChunks;
+  chunking(paths, &chunkPaths, &nChunks);
+  std::vector<cltk_partial> host(I.nOut);
+  unsigned long long key = ~0ULL;
+  if (I.nOut) {
+    ck(launchCombine(static_cast<const cltk_partial*>(partialsDev), nChunks, I.nOut, I.combined, s),
+       "combine launch");
+    ck(cudaMemcpyAsync(host.data(), I.combined, I.nOut * sizeof(cltk_partial),
+                       cudaMemcpyDeviceToHost, s),
+       "cudaMemcpyAsync D2H");
+  }
+  ck(cudaMemcpyAsync(&key, I.errKey, sizeof key, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+  ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  ck(cudaMemsetAsync(I.errKey, 0xff, sizeof(unsigned long long), s), "cudaMemsetAsync");
+  if (key != ~0ULL) {
+    const uint32_t site = static_cast<uint32_t>(key & 0xffffff);
+    const ErrorSite& e = site < I.prog.sites.size() ? I.prog.sites[site]
+                                                     : ErrorSite{ErrorCode::Eval, "device error"};
+    throw Error(e.code, e.message);
+  }
+  const cltk_plan_header& h = I.prog.header;
+  std::vector<PriceResult> out;
+  out.reserve(I.nOut);
+  for (uint32_t i = 0; i < h.n_instances; ++i)
+    for (uint32_t d = 0; d < h.n_days; ++d) {
+      const cltk_partial& p = host[i * h.n_days + d];
+      PriceResult r;
+      r.paths = paths;
+      r.seed = seed;
+      r.valuationDay = 0;
+      r.price = p.mean;
+      // stdError = sqrt(var / n), var = sum (x - mean)^2 / (n - 1)
+      // (proj/src/pricing.cpp:296-305)
+      r.stdError = p.n > 1.0 ? std::sqrt((p.m2 / (p.n - 1.0)) / p.n) : 0.0;
+      out.push_back(r);
+    }
+  return out;
+}
+
+std::string Plan::dump() const { return impl_->prog.listing; }
+
+uint64_t planErrorWord(Plan& plan, void* stream) {
+  PlanImpl& I = *plan.impl();
+  PlanImpl::DeviceGuard g(I.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long key = ~0ULL;
+  ck(cudaMemcpyAsync(&key, I.errKey, sizeof key, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+  ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  return key;
+}
+
+void planSetErrorWord(Plan& plan, void* stream, uint64_t word) {
+  PlanImpl& I = *plan.impl();
+  PlanImpl::DeviceGuard g(I.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long key = word;
+  ck(cudaMemcpyAsync(I.errKey, &key, sizeof key, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+  ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+uint64_t debugPaths(Plan& plan, uint64_t seed, uint64_t path0, uint64_t npaths, double* outputs,
+                    double* spots, double* normals) {
+  PlanImpl& I = *plan.impl();
+  PlanImpl::DeviceGuard g(I.device);
+  const cltk_plan_header& h = I.prog.header;
+  const size_t nS = static_cast<size_t>(npaths) * h.n_steps * std::max<uint32_t>(1, h.n_assets);
+  const size_t nO = static_cast<size_t>(npaths) * I.nOut;
+  double *dO = nullptr, *dS = nullptr, *dZ = nullptr;
+  unsigned long long* dE = nullptr;
+  ck(cudaMalloc(&dE, sizeof *dE), "cudaMalloc");
+  ck(cudaMemset(dE, 0xff, sizeof *dE), "cudaMemset");
+  if (outputs && nO) ck(cudaMalloc(&dO, nO * sizeof(double)), "cudaMalloc");
+  if (spots && nS) ck(cudaMalloc(&dS, nS * sizeof(double)), "cudaMalloc");
+  if (normals && nS) ck(cudaMalloc(&dZ, nS * sizeof(double)), "cudaMalloc");
+  if (dZ) ck(cudaMemset(dZ, 0, nS * sizeof(double)), "cudaMemset");
+  DumpArgs a{seed, path0, npaths, dS, dO, dZ, dE};
+  ck(launchDump(I.dev, a, nullptr), "dump launch");
+  ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  if (dO) ck(cudaMemcpy(outputs, dO, nO * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  if (dS) ck(cudaMemcpy(spots, dS, nS * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  if (dZ) ck(cudaMemcpy(normals, dZ, nS * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  unsigned long long key = ~0ULL;
+  ck(cudaMemcpy(&key, dE, sizeof key, cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(dO);
+  cudaFree(dS);
+  cudaFree(dZ);
+  cudaFree(dE);
+  return key;
+}
+
+void debugRng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n, uint64_t* bits,
+              double* uniforms, double* normals) {
+  if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+  uint64_t* dB = nullptr;
+  double *dU = nullptr, *dN = nullptr;
+  ck(cudaMalloc(&dB, n * sizeof(uint64_t)), "cudaMalloc");
+  ck(cudaMalloc(&dU, n * sizeof(double)), "cudaMalloc");
+  ck(cudaMalloc(&dN, n * sizeof(double)), "cudaMalloc");
+  ck(launchRngDump(seed, path, i0, n, dB, dU, dN, nullptr), "rng launch");
+  ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  if (bits) ck(cudaMemcpy(bits, dB, n * sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+  if (uniforms) ck(cudaMemcpy(uniforms, dU, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  if (normals) ck(cudaMemcpy(normals, dN, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(dB);
+  cudaFree(dU);
+  cudaFree(dN);
+}
+
+double fp64Peak(int device, int iters, double* seconds) {
+  if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+  int dev = 0, sms = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+  double* sink = nullptr;
+  ck(cudaMalloc(&sink, 256 * sizeof(double)), "cudaMalloc");
+  const int grid = sms * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  ck(launchFp64Peak(sink, 16, grid, nullptr), "fp64 warmup");
+  cudaEventRecord(e0);
+  ck(launchFp64Peak(sink, iters, grid, nullptr), "fp64 launch");
+  cudaEventRecord(e1);
+  ck(cudaEventSynchronize(e1), "cudaEventSynchronize");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double flops = 2.0 * 16 * 8 * static_cast<double>(iters) * grid * 256;
+  if (seconds) *seconds = ms * 1e-3;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
+// ---- one-shot pricing on the plan's own buffers ----------------------------
+namespace {
+
+std::vector<PriceResult> runOnce(Plan& plan, uint64_t paths, uint64_t seed,
+                                 const std::vector<uint64_t>& days) {
+  PlanImpl& I = *plan.impl();
+  PlanImpl::DeviceGuard g(I.device);
+  uint64_t chunkPaths, nChunks;
+  plan.chunking(paths, &chunkPaths, &nChunks);
+  if (nChunks > I.ownPartialsChunks) {
+    if (I.ownPartials) cudaFree(I.ownPartials);
+    ck(cudaMalloc(&I.ownPartials, nChunks * std::max<uint32_t>(1, I.nOut) * sizeof(cltk_partial)),
+       "cudaMalloc partials");
+    I.ownPartialsChunks = nChunks;
+  }
+  cudaStream_t s = nullptr;
+  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+  std::vector<PriceResult> r;
+  try {
+    plan.launch(paths, seed, 0, nChunks, I.ownPartials, s);
+    r = plan.finalize(paths, seed, I.ownPartials, s);
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  cudaStreamDestroy(s);
+  const uint32_t nd = static_cast<uint32_t>(days.size());
+  for (std::size_t i = 0; i < r.size(); ++i) r[i].valuationDay = days[i % nd];
+  return r;
+}
+
+}  // namespace
+
+std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,
+                                    const ModelSpec& model, uint64_t paths, uint64_t seed,
+                                    const std::vector<uint64_t>& days, const TEnv& tenv,
+                                    const RunOptions& opt) {
+  if (paths == 0) throw EvalError("path count must be positive");
+  if (days.empty()) return {};
+  Plan plan(instances, model, days, tenv, opt);
+  return runOnce(plan, paths, seed, days);
+}
+
+std::vector<PriceResult> priceAcrossTime(const Kernel& k, const ModelSpec& model,
+                                         uint64_t paths, uint64_t seed,
+                                         const std::vector<uint64_t>& days, const TEnv& tenv,
+                                         unsigned /*threads*/) {
+  return priceBatch({&k}, model, paths, seed, days, tenv, RunOptions());
+}
+
+PriceResult priceMC(const Kernel& k, const ModelSpec& model, uint64_t paths, uint64_t seed,
+                    uint64_t valuationDay, const TEnv& tenv, unsigned threads) {
+  return priceAcrossTime(k, model, paths, seed, {valuationDay}, tenv, threads).front();
+}
+
+}  // namespace b200
+}  // namespace cltk

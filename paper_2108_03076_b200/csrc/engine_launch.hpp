@@ -1,0 +1,59 @@
+// Host-side launch wrappers for the sm_100a kernels in mc_engine.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "program.h"
+
+namespace cltk {
+namespace b200 {
+
+constexpr int kBlock = 128;  // threads per CTA (4 warps)
+constexpr int kWarps = kBlock / 32;
+
+// Everything the path kernel reads, all device pointers.
+struct DevPlan {
+  cltk_plan_header hdr;
+  const cltk_step* steps;
+  const uint64_t* code;
+  const double* sharedConst;
+  const double* instConst;
+  const cltk_output* outputs;
+};
+
+struct RunArgs {
+  uint64_t seed;
+  uint64_t paths;        // total paths of the run (whole job, all GPUs)
+  uint64_t chunkPaths;   // kBlock * ppt
+  uint32_t ppt;          // paths per thread per chunk
+  uint64_t c0, c1;       // chunk range handled by this launch
+  cltk_partial* partials;           // [n_chunks][n_out]
+  unsigned long long* errKey;       // min(path << 24 | site)
+  unsigned long long* chunkCounter; // dynamic chunk scheduler
+  double* accScratch;               // global accumulators when n_out is large
+};
+
+// Dump modes (tests): per-path outputs instead of reduction.
+struct DumpArgs {
+  uint64_t seed, path0, npaths;
+  double* spots;    // [npaths][n_steps][n_assets] or null
+  double* outputs;  // [npaths][n_out] or null
+  double* normals;  // [npaths][n_steps][n_assets] or null
+  unsigned long long* errKey;
+};
+
+size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem);
+bool accFitsSmem(const cltk_plan_header& h);
+// Blocks per SM the path kernel achieves for this plan (occupancy API).
+int pathKernelOccupancy(const cltk_plan_header& h, size_t smem);
+cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
+                       cudaStream_t s);
+cudaError_t launchCombine(const cltk_partial* parts, uint64_t nChunks, uint32_t nOut,
+                          cltk_partial* out, cudaStream_t s);
+cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s);
+cudaError_t launchRngDump(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
+                          uint64_t* bits, double* uniform, double* normal, cudaStream_t s);
+cudaError_t launchFp64Peak(double* sink, int iters, int grid, cudaStream_t s);
+
+}  // namespace b200
+}  // namespace cltk

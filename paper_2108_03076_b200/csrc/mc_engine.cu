@@ -1,0 +1,559 @@
+// sm_100a Monte Carlo pricing engine: one fused kernel per path.
+//
+//   Philox2x64-10 (proj/src/pricing.cpp:73-98)
+//     -> uniform (:100-103) -> Acklam + Halley inverse normal (:109-148)
+//     -> Cholesky-correlated exact GBM step over the sorted day grid (:214-245)
+//     -> streaming payoff program (compiler.cpp; evalKernel semantics,
+//        proj/src/kernel.cpp:229-310) run as each day's spots appear
+//     -> shifted-sum warp partials -> per-chunk (n, mean, M2)
+//   then a fixed-order combine kernel (replaces pairwiseSum/reduce,
+//   proj/src/pricing.cpp:256-307).
+//
+// FP64 arithmetic that the reference performs unfused is written with
+// __dadd_rn/__dmul_rn (never contracted into DFMA) and the file is compiled
+// with -fmad=false, so every operation rounds exactly as the x86-64 reference
+// does; exp/log/erfc are the CUDA libdevice routines (a few ulp from glibc).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "engine_launch.hpp"
+#include "program.h"
+
+namespace cltk {
+namespace b200 {
+
+namespace {
+
+constexpr uint64_t kPhiloxM = 0xD2B74407B1CE6E93ULL;
+constexpr uint64_t kPhiloxW = 0x9E3779B97F4A7C15ULL;
+constexpr unsigned long long kNoError = ~0ULL;
+
+// ---------------------------------------------------------------------------
+// RNG: Random123 philox2x64-10, ctr = (i, path), key = seed, out c0 ^ c1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t philox_bits(uint64_t seed, uint64_t i, uint64_t path) {
+  uint64_t c0 = i, c1 = path, key = seed;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint64_t hi = __umul64hi(kPhiloxM, c0);
+    uint64_t lo = kPhiloxM * c0;
+    c0 = hi ^ key ^ c1;
+    c1 = lo;
+    key += kPhiloxW;
+  }
+  return c0 ^ c1;
+}
+
+// (double(bits >> 11) + 0.5) * 2^-53  -- exact conversion, one rounding add.
+__device__ __forceinline__ double uniform_of(uint64_t bits) {
+  return __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
+}
+
+// ---------------------------------------------------------------------------
+// invNormalCdf (proj/src/pricing.cpp:111-148), operation order preserved.
+// ---------------------------------------------------------------------------
+#define M_ __dmul_rn
+#define A_ __dadd_rn
+
+__device__ __forceinline__ double inv_normal(double p) {
+  const double a0 = -3.969683028665376e+01, a1 = 2.209460984245205e+02,
+               a2 = -2.759285104469687e+02, a3 = 1.383577518672690e+02,
+               a4 = -3.066479806614716e+01, a5 = 2.506628277459239e+00;
+  const double b0 = -5.447609879822406e+01, b1 = 1.615858368580409e+02,
+               b2 = -1.556989798598866e+02, b3 = 6.680131188771972e+01,
+               b4 = -1.328068155288572e+01;
+  const double c0 = -7.784894002430293e-03, c1 = -3.223964580411365e-01,
+               c2 = -2.400758277161838e+00, c3 = -2.549732539343734e+00,
+               c4 = 4.374664141464968e+00, c5 = 2.938163982698783e+00;
+  const double d0 = 7.784695709041462e-03, d1 = 3.224671290700398e-01,
+               d2 = 2.445134137142996e+00, d3 = 3.754408661907416e+00;
+  const double plow = 0.02425;
+  const double phigh = 0x1.f395810624dd3p-1;  // 1.0 - plow, as the reference folds it
+  double x;
+  if (p >= plow && p <= phigh) {
+    double q = A_(p, -0.5);
+    double r = M_(q, q);
+    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(a0, r), a1), r), a2), r), a3), r), a4), r), a5);
+    double den = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(b0, r), b1), r), b2), r), b3), r), b4), r), 1.0);
+    x = __ddiv_rn(M_(num, q), den);
+  } else {
+    bool lower = p < plow;
+    double q = __dsqrt_rn(M_(-2.0, log(lower ? p : A_(1.0, -p))));
+    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(c0, q), c1), q), c2), q), c3), q), c4), q), c5);
+    double den = A_(M_(A_(M_(A_(M_(A_(M_(d0, q), d1), q), d2), q), d3), q), 1.0);
+    x = __ddiv_rn(lower ? num : -num, den);
+  }
+  // Halley step: e = 0.5*erfc(-x/sqrt(2)) - p; u = e*sqrt(2*pi)*exp(x*x/2)
+  const double kSqrt2 = 0x1.6a09e667f3bcdp+0;    // std::sqrt(2.0)
+  const double kSqrt2Pi = 0x1.40d931ff62705p+1;  // std::sqrt(2.0 * M_PI)
+  double e = A_(M_(0.5, erfc(__ddiv_rn(-x, kSqrt2))), -p);
+  double u = M_(M_(e, kSqrt2Pi), exp(M_(M_(x, x), 0.5)));
+  return A_(x, -__ddiv_rn(u, A_(1.0, M_(M_(x, u), 0.5))));
+}
+
+// ---------------------------------------------------------------------------
+// Payoff program interpreter (operand space: program.h).
+// ---------------------------------------------------------------------------
+struct Frame {
+  double* R;        // this thread's register column: operand r at R[r * kBlock]
+  const double* C;  // this warp's constant table, pre-offset by -n_thread
+  uint32_t nThread;
+};
+
+__device__ __forceinline__ double ld(const Frame f, uint32_t idx) {
+  return idx < f.nThread ? f.R[idx * kBlock] : f.C[idx];
+}
+
+__device__ __forceinline__ int64_t bits_of(double v) { return __double_as_longlong(v); }
+__device__ __forceinline__ double of_bits(int64_t v) { return __longlong_as_double(v); }
+
+__device__ __noinline__ void run_ops(const Frame f, const uint64_t* __restrict__ code,
+                                     uint32_t begin, uint32_t end) {
+  for (uint32_t pc = begin; pc < end; ++pc) {
+    const uint64_t w = __ldg(code + pc);
+    const uint32_t op = static_cast<uint32_t>(w & 0xff);
+    const uint32_t d = static_cast<uint32_t>(w >> 8) & 0x3fff;
+    const double va = ld(f, static_cast<uint32_t>(w >> 22) & 0x3fff);
+    const double vb = ld(f, static_cast<uint32_t>(w >> 36) & 0x3fff);
+    double r;
+    switch (op) {
+      case OP_MOV: r = va; break;
+      case OP_NEG: r = -va; break;
+      case OP_NOT: r = va == 0.0 ? 1.0 : 0.0; break;
+      case OP_ADD: r = __dadd_rn(va, vb); break;
+      case OP_SUB: r = __dsub_rn(va, vb); break;
+      case OP_MUL: r = __dmul_rn(va, vb); break;
+      case OP_DIV: r = __ddiv_rn(va, vb); break;
+      case OP_LT: r = va < vb ? 1.0 : 0.0; break;
+      case OP_LEQ: r = va <= vb ? 1.0 : 0.0; break;
+      case OP_EQ: r = va == vb ? 1.0 : 0.0; break;
+      case OP_AND: r = (va != 0.0 && vb != 0.0) ? 1.0 : 0.0; break;
+      case OP_OR: r = (va != 0.0 || vb != 0.0) ? 1.0 : 0.0; break;
+      case OP_SEL: r = va != 0.0 ? vb : ld(f, static_cast<uint32_t>(w >> 50) & 0x3fff); break;
+      case OP_IADD:
+        r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) +
+                                         static_cast<uint64_t>(bits_of(vb))));
+        break;
+      case OP_ISUB:
+        r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) -
+                                         static_cast<uint64_t>(bits_of(vb))));
+        break;
+      case OP_ILT: r = bits_of(va) < bits_of(vb) ? 1.0 : 0.0; break;
+      case OP_ILEQ: r = bits_of(va) <= bits_of(vb) ? 1.0 : 0.0; break;
+      case OP_IEQ: r = bits_of(va) == bits_of(vb) ? 1.0 : 0.0; break;
+      case OP_MIN: r = fmin(va, vb); break;
+      case OP_MAX: r = fmax(va, vb); break;
+      case OP_MINP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                 : fmin(va, vb);
+        break;
+      case OP_MAXP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                 : fmax(va, vb);
+        break;
+      case OP_EFIRST: r = bits_of(va) != 0 ? va : vb; break;
+      case OP_EDIVZ: r = va == 0.0 ? of_bits(static_cast<int64_t>(w >> 50)) : 0.0; break;
+      default: r = 0.0; break;
+    }
+    f.R[d * kBlock] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One path: simulate the day grid and run each step's payoff ops.
+// Returns false (and records nothing) on an invNormalCdf domain error; the
+// caller reports it.
+// ---------------------------------------------------------------------------
+template <int NA, bool DUMP>
+__device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, uint64_t seed,
+                                         uint64_t path, double* dumpS, double* dumpZ) {
+  const cltk_plan_header& h = P.hdr;
+  double logS[NA];
+  double L[NA][NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) {
+    logS[j] = h.logS0[j];
+#pragma unroll
+    for (int l = 0; l < NA; ++l) L[j][l] = h.chol[j * CLTK_MAX_ASSETS + l];
+  }
+  bool ok = true;
+  const uint32_t used = h.used_mask;
+  for (uint32_t s = 0; s < h.n_steps; ++s) {
+    const cltk_step* st = P.steps + s;
+    const uint32_t kind = __ldg(&st->draws);
+    double S[NA];
+    if (kind == 1) {
+      double raw[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        const uint64_t b = philox_bits(seed, static_cast<uint64_t>(s) * NA + j, path);
+        ok = ok && ((b >> 11) != 0x1FFFFFFFFFFFFFULL);  // uniform() == 1.0
+        raw[j] = inv_normal(uniform_of(b));
+      }
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l <= j; ++l) acc = __dadd_rn(acc, __dmul_rn(L[j][l], raw[l]));
+        logS[j] = __dadd_rn(logS[j], __dadd_rn(__ldg(&st->A[j]), __dmul_rn(__ldg(&st->B[j]), acc)));
+        S[j] = ((used >> j) & 1u) ? exp(logS[j]) : 0.0;
+        if (DUMP && dumpZ) dumpZ[s * NA + j] = raw[j];
+      }
+    } else if (kind == 0) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) S[j] = __ldg(&st->S[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) S[j] = ((used >> j) & 1u) ? exp(logS[j]) : 0.0;
+    }
+    if (DUMP && dumpS) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) dumpS[s * NA + j] = S[j];
+    }
+    const uint32_t cb = __ldg(&st->code_begin), ce = __ldg(&st->code_end);
+    if (cb < ce) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) f.R[j * kBlock] = S[j];
+      run_ops(f, P.code, cb, ce);
+    }
+  }
+  return ok;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Chan et al. pairwise combination of (n, mean, M2).
+__device__ __forceinline__ void chan(double& n, double& mean, double& m2, double nb,
+                                     double meanb, double m2b) {
+  if (nb == 0.0) return;
+  if (n == 0.0) {
+    n = nb;
+    mean = meanb;
+    m2 = m2b;
+    return;
+  }
+  const double nn = n + nb;
+  const double delta = meanb - mean;
+  mean = mean + delta * (nb / nn);
+  m2 = m2 + m2b + delta * delta * (n * nb / nn);
+  n = nn;
+}
+
+// Shared memory: [regs n_thread*kBlock][wconst kWarps*(nc+ni)][acc ...][misc]
+template <int NA>
+__global__ void __launch_bounds__(kBlock) path_kernel(const DevPlan P, const RunArgs A,
+                                                      int accInSmem) {
+  extern __shared__ double smem[];
+  const cltk_plan_header& h = P.hdr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nc = h.n_shared_const, ni = h.n_inst_const;
+  const uint32_t nOut = h.n_instances * h.n_days;
+  double* regs = smem;
+  double* wconst = regs + static_cast<size_t>(h.n_thread) * kBlock + warp * (nc + ni);
+  double* accBase = smem + static_cast<size_t>(h.n_thread) * kBlock + kWarps * (nc + ni);
+  // acc layout per warp: [nOut][3] (K, s1, s2); counts[kWarps] after.
+  double* acc;
+  double* counts;
+  if (accInSmem) {
+    acc = accBase + static_cast<size_t>(warp) * nOut * 3;
+    counts = accBase + static_cast<size_t>(kWarps) * nOut * 3;
+  } else {
+    acc = A.accScratch + (static_cast<size_t>(blockIdx.x) * kWarps + warp) * nOut * 3;
+    counts = accBase;
+  }
+  unsigned long long* chunkSlot =
+      reinterpret_cast<unsigned long long*>(counts + kWarps);
+
+  for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
+  __syncwarp();
+  Frame f{regs + tid, wconst - h.n_thread, h.n_thread};
+
+  for (;;) {
+    if (tid == 0) *chunkSlot = A.c0 + atomicAdd(A.chunkCounter, 1ULL);
+    __syncthreads();
+    const uint64_t chunk = *chunkSlot;
+    if (chunk >= A.c1) break;
+    for (uint32_t i = lane; i < nOut * 3; i += 32) acc[i] = 0.0;
+    if (lane == 0) counts[warp] = 0.0;
+    __syncwarp();
+
+    const uint64_t base = chunk * A.chunkPaths;
+    for (uint32_t k = 0; k < A.ppt; ++k) {
+      const uint64_t path = base + static_cast<uint64_t>(k) * kBlock + tid;
+      const bool active = path < A.paths;
+      if (__all_sync(0xffffffffu, !active)) continue;  // warp-uniform
+      const uint64_t p = active ? path : A.paths - 1;
+      bool ok = simulate<NA, false>(P, f, A.seed, p, nullptr, nullptr);
+      if (active && !ok) atomicMin(A.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
+      const uint32_t nAct = __popc(__ballot_sync(0xffffffffu, active));
+      const bool first = counts[warp] == 0.0;
+      for (uint32_t inst = 0; inst < h.n_instances; ++inst) {
+        if (ni) {
+          __syncwarp();
+          for (uint32_t i = lane; i < ni; i += 32)
+            wconst[nc + i] = __ldg(P.instConst + static_cast<size_t>(inst) * ni + i);
+          __syncwarp();
+        }
+        if (h.inst_code_begin < h.inst_code_end)
+          run_ops(f, P.code, h.inst_code_begin, h.inst_code_end);
+        for (uint32_t d = 0; d < h.n_days; ++d) {
+          const cltk_output o = P.outputs[d];
+          const double v = ld(f, o.val);
+          if (h.has_err && o.err != CLTK_NO_ERR) {
+            const int64_t e = bits_of(ld(f, o.err));
+            if (active && e != 0)
+              atomicMin(A.errKey, (static_cast<unsigned long long>(p) << 24) |
+                                      static_cast<unsigned long long>(e));
+          }
+          double* a = acc + static_cast<size_t>(inst * h.n_days + d) * 3;
+          double K;
+          if (first) {
+            K = __shfl_sync(0xffffffffu, v, 0);
+          } else {
+            K = a[0];
+          }
+          const double dv = active ? v - K : 0.0;
+          const double s1 = warp_sum(dv);
+          const double s2 = warp_sum(dv * dv);
+          if (lane == 0) {
+            if (first) a[0] = K;
+            a[1] += s1;
+            a[2] += s2;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) counts[warp] += static_cast<double>(nAct);
+      __syncwarp();
+    }
+    __syncthreads();
+    // Chunk partial: combine the warps in fixed order.
+    for (uint32_t o = tid; o < nOut; o += kBlock) {
+      double n = 0.0, mean = 0.0, m2 = 0.0;
+      for (int w = 0; w < kWarps; ++w) {
+        const double nw = counts[w];
+        if (nw == 0.0) continue;
+        const double* a = accInSmem ? accBase + (static_cast<size_t>(w) * nOut + o) * 3
+                                    : A.accScratch +
+                                          ((static_cast<size_t>(blockIdx.x) * kWarps + w) * nOut + o) * 3;
+        const double s1 = a[1], s2 = a[2];
+        const double mw = a[0] + s1 / nw;
+        double m2w = s2 - s1 * (s1 / nw);
+        if (m2w < 0.0) m2w = 0.0;
+        chan(n, mean, m2, nw, mw, m2w);
+      }
+      cltk_partial* out = A.partials + chunk * nOut + o;
+      out->n = n;
+      out->mean = mean;
+      out->m2 = m2;
+    }
+    __syncthreads();
+  }
+}
+
+// Fixed-order combine: block per output; thread t folds a contiguous range
+// sequentially, then a fixed tree.  Depends only on n_chunks (G-invariant).
+__global__ void __launch_bounds__(256) combine_kernel(const cltk_partial* __restrict__ parts,
+                                                      uint64_t nChunks, uint32_t nOut,
+                                                      cltk_partial* out) {
+  __shared__ double sn[256], sm[256], s2[256];
+  const uint32_t o = blockIdx.x;
+  const uint64_t per = (nChunks + 255) / 256;
+  const uint64_t lo = threadIdx.x * per, hi = min(nChunks, lo + per);
+  double n = 0.0, mean = 0.0, m2 = 0.0;
+  for (uint64_t c = lo; c < hi; ++c) {
+    const cltk_partial p = parts[c * nOut + o];
+    chan(n, mean, m2, p.n, p.mean, p.m2);
+  }
+  sn[threadIdx.x] = n;
+  sm[threadIdx.x] = mean;
+  s2[threadIdx.x] = m2;
+  __syncthreads();
+  for (int stride = 128; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) {
+      double a = sn[threadIdx.x], b = sm[threadIdx.x], c = s2[threadIdx.x];
+      chan(a, b, c, sn[threadIdx.x + stride], sm[threadIdx.x + stride], s2[threadIdx.x + stride]);
+      sn[threadIdx.x] = a;
+      sm[threadIdx.x] = b;
+      s2[threadIdx.x] = c;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[o].n = sn[0];
+    out[o].mean = sm[0];
+    out[o].m2 = s2[0];
+  }
+}
+
+// Per-path dump (tests): same simulate/interpret code, outputs written out.
+template <int NA>
+__global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const DumpArgs D) {
+  extern __shared__ double smem[];
+  const cltk_plan_header& h = P.hdr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nc = h.n_shared_const, ni = h.n_inst_const;
+  const uint32_t nOut = h.n_instances * h.n_days;
+  double* wconst = smem + static_cast<size_t>(h.n_thread) * kBlock + warp * (nc + ni);
+  for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
+  __syncwarp();
+  Frame f{smem + tid, wconst - h.n_thread, h.n_thread};
+  const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kBlock + tid;
+  const bool active = idx < D.npaths;
+  const uint64_t q = active ? idx : 0;
+  const uint64_t p = D.path0 + q;
+  const size_t sz = static_cast<size_t>(h.n_steps) * NA;
+  bool ok = simulate<NA, true>(P, f, D.seed, p, D.spots ? D.spots + q * sz : nullptr,
+                               D.normals ? D.normals + q * sz : nullptr);
+  if (active && !ok) atomicMin(D.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
+  for (uint32_t inst = 0; inst < h.n_instances; ++inst) {
+    if (ni) {
+      __syncwarp();
+      for (uint32_t i = lane; i < ni; i += 32)
+        wconst[nc + i] = __ldg(P.instConst + static_cast<size_t>(inst) * ni + i);
+      __syncwarp();
+    }
+    if (h.inst_code_begin < h.inst_code_end) run_ops(f, P.code, h.inst_code_begin, h.inst_code_end);
+    for (uint32_t d = 0; d < h.n_days; ++d) {
+      const cltk_output o = P.outputs[d];
+      const double v = ld(f, o.val);
+      if (h.has_err && o.err != CLTK_NO_ERR) {
+        const int64_t e = bits_of(ld(f, o.err));
+        if (active && e != 0)
+          atomicMin(D.errKey, (static_cast<unsigned long long>(p) << 24) |
+                                  static_cast<unsigned long long>(e));
+      }
+      if (active && D.outputs) D.outputs[q * nOut + inst * h.n_days + d] = v;
+    }
+  }
+}
+
+__global__ void rng_kernel(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n, uint64_t* bits,
+                           double* uni, double* nor) {
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint64_t b = philox_bits(seed, i0 + k, path);
+  const double u = uniform_of(b);
+  if (bits) bits[k] = b;
+  if (uni) uni[k] = u;
+  if (nor) nor[k] = inv_normal(u);
+}
+
+// DFMA throughput probe: 8 independent chains per thread.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* sink, int iters) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = 1.0 + 1e-9 * (threadIdx.x + i);
+  const double a = 0.999999999, b = 1e-12;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.678) sink[threadIdx.x] = s;
+}
+
+template <int NA>
+cudaError_t launchPathT(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
+                        cudaStream_t s, int accInSmem) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(path_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  path_kernel<NA><<<grid, kBlock, smem, s>>>(p, a, accInSmem);
+  return cudaGetLastError();
+}
+
+template <int NA>
+cudaError_t launchDumpT(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
+  const cltk_plan_header& h = p.hdr;
+  size_t smem = (static_cast<size_t>(h.n_thread) * kBlock +
+                 kWarps * (h.n_shared_const + h.n_inst_const)) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(dump_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = static_cast<unsigned>((a.npaths + kBlock - 1) / kBlock);
+  dump_kernel<NA><<<grid, kBlock, smem, s>>>(p, a);
+  return cudaGetLastError();
+}
+
+template <int NA>
+int occupancyT(size_t smem) {
+  int blocks = 0;
+  cudaFuncSetAttribute(path_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, path_kernel<NA>, kBlock, smem);
+  return blocks;
+}
+
+}  // namespace
+
+bool accFitsSmem(const cltk_plan_header& h) {
+  const size_t nOut = static_cast<size_t>(h.n_instances) * h.n_days;
+  return kWarps * nOut * 3 * sizeof(double) <= 48 * 1024;
+}
+
+size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
+  const size_t nOut = static_cast<size_t>(h.n_instances) * h.n_days;
+  size_t words = static_cast<size_t>(h.n_thread) * kBlock + kWarps * (h.n_shared_const + h.n_inst_const);
+  if (accInSmem) words += kWarps * nOut * 3;
+  words += kWarps + 1;  // counts + chunk slot
+  return words * sizeof(double);
+}
+
+#define CLTK_NA_SWITCH(NA_, CALL)                 \
+  switch (NA_) {                                  \
+    case 1: { constexpr int NA = 1; CALL; }       \
+    case 2: { constexpr int NA = 2; CALL; }       \
+    case 3: { constexpr int NA = 3; CALL; }       \
+    case 4: { constexpr int NA = 4; CALL; }       \
+    case 5: { constexpr int NA = 5; CALL; }       \
+    case 6: { constexpr int NA = 6; CALL; }       \
+    case 7: { constexpr int NA = 7; CALL; }       \
+    case 8: { constexpr int NA = 8; CALL; }       \
+    default: { constexpr int NA = 1; CALL; }      \
+  }
+
+int pathKernelOccupancy(const cltk_plan_header& h, size_t smem) {
+  CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return occupancyT<NA>(smem));
+}
+
+cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem, cudaStream_t s) {
+  const int accInSmem = accFitsSmem(p.hdr) ? 1 : 0;
+  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
+                 return launchPathT<NA>(p, a, grid, smem, s, accInSmem));
+}
+
+cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
+  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return launchDumpT<NA>(p, a, s));
+}
+
+cudaError_t launchCombine(const cltk_partial* parts, uint64_t nChunks, uint32_t nOut,
+                          cltk_partial* out, cudaStream_t s) {
+  combine_kernel<<<nOut, 256, 0, s>>>(parts, nChunks, nOut, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launchRngDump(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n, uint64_t* bits,
+                          double* uniform, double* normal, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+  rng_kernel<<<grid, 256, 0, s>>>(seed, path, i0, n, bits, uniform, normal);
+  return cudaGetLastError();
+}
+
+cudaError_t launchFp64Peak(double* sink, int iters, int grid, cudaStream_t s) {
+  fp64_peak_kernel<<<grid, 256, 0, s>>>(sink, iters);
+  return cudaGetLastError();
+}
+
+}  // namespace b200
+}  // namespace cltk

@@ -1,0 +1,110 @@
+// Device program format shared by the host payoff compiler (compiler.cpp) and
+// the sm_100a Monte Carlo engine (mc_engine.cu).
+//
+// A compiled payoff is a *streaming* three-address program over per-thread
+// registers: every instruction is attached to the simulation step (sorted
+// distinct kernel day, SimPlan::days in proj/src/pricing.cpp:182-190) at
+// which all of its observable inputs exist, so the engine interleaves payoff
+// evaluation with path generation and never materialises ext[rows][cols]
+// (proj/src/pricing.cpp:247-251) anywhere -- not in HBM, not in shared memory.
+//
+// Operand space (14-bit indices):
+//   [0, n_assets)             S-slots: this step's spot per model asset
+//   [n_assets, n_thread)      thread registers
+//   [n_thread, n_thread+n_shared_const)            warp-broadcast constants
+//   [n_thread+n_shared_const, ... + n_inst_const)  per-instance constants
+// Thread registers live in shared memory, register-major
+// (reg * BLOCK + tid) so a warp touches 32 consecutive doubles; constants live
+// in a per-warp shared-memory table read as a broadcast.
+#pragma once
+#include <stdint.h>
+
+#define CLTK_OP_BITS 8
+#define CLTK_FIELD_BITS 14
+#define CLTK_MAX_OPERANDS (1 << CLTK_FIELD_BITS)
+#define CLTK_MAX_ASSETS 8
+
+// Value kinds in the 8-byte register slots: R = IEEE double; B = double 0/1;
+// I = int64 bit pattern (KExpr int values, proj/src/kernel.cpp:187);
+// E = int64 error-site index (0 = no error).
+enum cltk_opcode : uint32_t {
+  OP_NOP = 0,
+  OP_MOV,      // d = a
+  OP_NEG,      // R: d = -a
+  OP_NOT,      // B: d = !a
+  OP_ADD,      // R: d = a + b (IEEE, never contracted)
+  OP_SUB,
+  OP_MUL,
+  OP_DIV,      // R: d = a / b  (zero divisor guarded by OP_EDIVZ)
+  OP_LT,       // R,R -> B
+  OP_LEQ,
+  OP_EQ,
+  OP_AND,      // B,B -> B
+  OP_OR,
+  OP_SEL,      // d = a ? b : c   (any kind; a is B)
+  OP_IADD,     // I: d = a + b (int64 wrap)
+  OP_ISUB,
+  OP_ILT,      // I,I -> B
+  OP_ILEQ,
+  OP_IEQ,
+  OP_MIN,      // R: fmin (NaN-ignoring)   -- OR/AND-of-compare rewrite
+  OP_MAX,      // R: fmax (NaN-ignoring)
+  OP_MINP,     // R: NaN-propagating min
+  OP_MAXP,     // R: NaN-propagating max
+  OP_EFIRST,   // E: d = a != 0 ? a : b
+  OP_EDIVZ,    // E: d = (a == 0.0) ? c(field) : 0   (c is an immediate site id)
+  OP_COUNT
+};
+
+// 64-bit instruction: op | d<<8 | a<<22 | b<<36 | c<<50
+static inline uint64_t cltk_encode(uint32_t op, uint32_t d, uint32_t a,
+                                   uint32_t b, uint32_t c) {
+  return (uint64_t)op | ((uint64_t)d << 8) | ((uint64_t)a << 22) |
+         ((uint64_t)b << 36) | ((uint64_t)c << 50);
+}
+
+// Per-step simulation constants (host-computed with glibc, bit-identical to
+// the reference's SimPlan arithmetic, proj/src/pricing.cpp:226-245).
+typedef struct {
+  double A[CLTK_MAX_ASSETS];  // (drift - 0.5*vol*vol) * dt
+  double B[CLTK_MAX_ASSETS];  // vol * sqrt(dt)
+  double S[CLTK_MAX_ASSETS];  // exp(log(spot)) when dt == 0 (path-independent)
+  uint32_t draws;             // 1: dt > 0 (draw nA normals), 0: dt == 0
+  uint32_t code_begin;        // shared-op range of this step
+  uint32_t code_end;
+  uint32_t pad;
+} cltk_step;
+
+// Launch-time header of a compiled plan (everything uniform across threads).
+typedef struct {
+  uint32_t n_assets;        // model assets (draws per step)
+  uint32_t n_steps;
+  uint32_t n_thread;        // S-slots + thread registers
+  uint32_t n_shared_const;
+  uint32_t n_inst_const;
+  uint32_t n_instances;
+  uint32_t n_days;          // valuation days
+  uint32_t inst_code_begin; // instance-op range (run once per instance)
+  uint32_t inst_code_end;
+  uint32_t has_err;         // any output carries an error register
+  uint32_t used_mask;       // model assets referenced by any kernel column
+  uint32_t pad;
+  double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
+  double logS0[CLTK_MAX_ASSETS];                   // log(spot)
+} cltk_plan_header;
+
+// Output slot: value operand and error operand (0xFFFF... = none) per
+// valuation day, evaluated after the instance ops of each instance.
+typedef struct {
+  uint32_t val;
+  uint32_t err;
+} cltk_output;
+
+#define CLTK_NO_ERR 0xFFFFFFFFu
+
+// Chunk partial of one output: count, mean, sum of squared deviations.
+typedef struct {
+  double n;
+  double mean;
+  double m2;
+} cltk_partial;
