@@ -31,7 +31,9 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 # FP64 flops per path of the fused kernel, frozen from the ncu SASS op counters
 # (dadd + dmul + 2*dfma) of the first correct kernel (profiles/).
-F_PATH = {"brc": None, "worst_off": None, "call": None}
+F_PATH = {"brc": 286221.4, "worst_off": None, "call": None}
+# brc: ncu r1 (profiles/r1_path_kernel_brc_2M_raw.csv), 2e6 paths:
+#   dadd 6.2471e10 + dmul 7.0817e10 + 2 * dfma 2.19577e11 thread-instructions
 
 WORKLOADS = {
     "brc": ("brc", "three", "BRC 3 underlyings x 367 dates (contracts/brc.cl, SURVEY.md App. A)"),
@@ -295,7 +297,8 @@ def main():
                                  f"{h2d} B compiled program",
                            "kernel_ms": t_kern},
                 "roofline": roof, "cpu_baseline": cpu,
-                "e2e": {"value": paths / t_e2e, "unit": "paths/s", "h2d_bytes_per_step": h2d,
+                "e2e": {"value": paths / t_e2e if t_e2e > 0 else None, "unit": "paths/s",
+                        "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h,
                         "path": "paper_2108_03076_b200.price -> cltk_gpu_price (C-ABI), host "
                                 "kernel/model JSON in, host results out"},

@@ -56,40 +56,46 @@ __device__ __forceinline__ double uniform_of(uint64_t bits) {
 #define M_ __dmul_rn
 #define A_ __dadd_rn
 
+// Coefficients live in the constant bank so DFMA/DMUL take them as c[][]
+// operands (immediates would be rematerialised with UMOV pairs per use).
+__constant__ double kAck[32] = {
+    // a0..a5 (central numerator)
+    -3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+    1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00,
+    // b0..b4 (central denominator)
+    -5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+    6.680131188771972e+01, -1.328068155288572e+01,
+    // c0..c5 (tail numerator)
+    -7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+    -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00,
+    // d0..d3 (tail denominator)
+    7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+    3.754408661907416e+00,
+    // 21: plow, 22: 1 - plow (as the reference folds it), 23: sqrt(2.0),
+    // 24: sqrt(2.0 * M_PI), 25: 0.5, 26: -0.5, 27: 1.0, 28: -2.0, 29: 2^-53
+    0.02425, 0x1.f395810624dd3p-1, 0x1.6a09e667f3bcdp+0, 0x1.40d931ff62705p+1,
+    0.5, -0.5, 1.0, -2.0, 0x1.0p-53, 0.0, 0.0};
+
 __device__ __forceinline__ double inv_normal(double p) {
-  const double a0 = -3.969683028665376e+01, a1 = 2.209460984245205e+02,
-               a2 = -2.759285104469687e+02, a3 = 1.383577518672690e+02,
-               a4 = -3.066479806614716e+01, a5 = 2.506628277459239e+00;
-  const double b0 = -5.447609879822406e+01, b1 = 1.615858368580409e+02,
-               b2 = -1.556989798598866e+02, b3 = 6.680131188771972e+01,
-               b4 = -1.328068155288572e+01;
-  const double c0 = -7.784894002430293e-03, c1 = -3.223964580411365e-01,
-               c2 = -2.400758277161838e+00, c3 = -2.549732539343734e+00,
-               c4 = 4.374664141464968e+00, c5 = 2.938163982698783e+00;
-  const double d0 = 7.784695709041462e-03, d1 = 3.224671290700398e-01,
-               d2 = 2.445134137142996e+00, d3 = 3.754408661907416e+00;
-  const double plow = 0.02425;
-  const double phigh = 0x1.f395810624dd3p-1;  // 1.0 - plow, as the reference folds it
+  const double* K = kAck;
   double x;
-  if (p >= plow && p <= phigh) {
-    double q = A_(p, -0.5);
+  if (p >= K[21] && p <= K[22]) {
+    double q = A_(p, K[26]);
     double r = M_(q, q);
-    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(a0, r), a1), r), a2), r), a3), r), a4), r), a5);
-    double den = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(b0, r), b1), r), b2), r), b3), r), b4), r), 1.0);
+    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[0], r), K[1]), r), K[2]), r), K[3]), r), K[4]), r), K[5]);
+    double den = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[6], r), K[7]), r), K[8]), r), K[9]), r), K[10]), r), K[27]);
     x = __ddiv_rn(M_(num, q), den);
   } else {
-    bool lower = p < plow;
-    double q = __dsqrt_rn(M_(-2.0, log(lower ? p : A_(1.0, -p))));
-    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(c0, q), c1), q), c2), q), c3), q), c4), q), c5);
-    double den = A_(M_(A_(M_(A_(M_(A_(M_(d0, q), d1), q), d2), q), d3), q), 1.0);
+    bool lower = p < K[21];
+    double q = __dsqrt_rn(M_(K[28], log(lower ? p : A_(K[27], -p))));
+    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[11], q), K[12]), q), K[13]), q), K[14]), q), K[15]), q), K[16]);
+    double den = A_(M_(A_(M_(A_(M_(A_(M_(K[17], q), K[18]), q), K[19]), q), K[20]), q), K[27]);
     x = __ddiv_rn(lower ? num : -num, den);
   }
   // Halley step: e = 0.5*erfc(-x/sqrt(2)) - p; u = e*sqrt(2*pi)*exp(x*x/2)
-  const double kSqrt2 = 0x1.6a09e667f3bcdp+0;    // std::sqrt(2.0)
-  const double kSqrt2Pi = 0x1.40d931ff62705p+1;  // std::sqrt(2.0 * M_PI)
-  double e = A_(M_(0.5, erfc(__ddiv_rn(-x, kSqrt2))), -p);
-  double u = M_(M_(e, kSqrt2Pi), exp(M_(M_(x, x), 0.5)));
-  return A_(x, -__ddiv_rn(u, A_(1.0, M_(M_(x, u), 0.5))));
+  double e = A_(M_(K[25], erfc(__ddiv_rn(-x, K[23]))), -p);
+  double u = M_(M_(e, K[24]), exp(M_(M_(x, x), K[25])));
+  return A_(x, -__ddiv_rn(u, A_(K[27], M_(M_(x, u), K[25]))));
 }
 
 // ---------------------------------------------------------------------------
@@ -183,11 +189,16 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, uint64
     double S[NA];
     if (kind == 1) {
       double raw[NA];
-#pragma unroll
+      // One normal at a time (rolled: keeps the inlined inverse-normal code
+      // once in the I-cache); raw[] stays in registers via the select.
+#pragma unroll 1
       for (int j = 0; j < NA; ++j) {
         const uint64_t b = philox_bits(seed, static_cast<uint64_t>(s) * NA + j, path);
         ok = ok && ((b >> 11) != 0x1FFFFFFFFFFFFFULL);  // uniform() == 1.0
-        raw[j] = inv_normal(uniform_of(b));
+        const double z = inv_normal(uniform_of(b));
+#pragma unroll
+        for (int q = 0; q < NA; ++q)
+          if (q == j) raw[q] = z;
       }
 #pragma unroll
       for (int j = 0; j < NA; ++j) {
