@@ -20,8 +20,8 @@ HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS)))
 CU_OBJS   := $(OBJ)/mc_engine.o
 HDRS      := $(wildcard $(SRC)/*.hpp $(SRC)/*.h) include/cltk_b200.h
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle testlib clean
+all: lib oracle testlib
 
 lib: $(LIB)
 
@@ -42,3 +42,9 @@ oracle:
 
 clean:
 	rm -rf build $(LIB)
+
+# test helper: host build of csrc/glibc_math.h (checked against the system libm)
+testlib: build/libgm_check.so
+build/libgm_check.so: tests/native/gm_check.cpp $(SRC)/glibc_math.h $(SRC)/glibc_tables.h
+	@mkdir -p build
+	$(HOSTCXX) -std=c++17 -O2 -fPIC -shared -ffp-contract=off -o $@ $< -lm

@@ -123,6 +123,10 @@ int cltk_debug_paths(cltk_plan* plan, uint64_t seed, uint64_t path0, uint64_t np
 /* Philox bits / uniforms / normals of stream (seed, path), indices [i0, i0+n). */
 int cltk_debug_rng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
                    uint64_t* bits, double* uniforms, double* normals, cltk_error* err);
+/* Device exp / log / erfc / invNormalCdf (fn = 0..3) of x[n] (host buffers):
+ * the engine's bit-exact restatements of glibc's routines. */
+int cltk_debug_math(int device, int fn, const double* x, uint64_t n, double* out,
+                    cltk_error* err);
 /* Measured DFMA throughput (TFLOP/s) over `iters` iterations. */
 int cltk_fp64_peak(int device, int iters, double* tflops, double* seconds, cltk_error* err);
 

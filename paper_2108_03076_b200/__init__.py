@@ -35,7 +35,7 @@ from . import _native
 __all__ = [
     "Kernel", "ContractError", "ContractParseError", "ContractTypeError",
     "ContractUnsupportedError", "price", "price_batch", "black_scholes_call", "Plan",
-    "compile_listing", "debug_rng", "fp64_peak", "load_kernel", "version",
+    "compile_listing", "debug_rng", "debug_math", "fp64_peak", "load_kernel", "version",
 ]
 
 
@@ -355,6 +355,20 @@ def debug_rng(seed: int, path: int, i0: int, n: int, device: int = -1):
                                       C.byref(err))
     _raise(rc, err)
     return bits, uni, nor
+
+
+def debug_math(fn: str, x, device: int = -1):
+    """Device build of the engine's glibc-exact ``exp`` / ``log`` / ``erfc`` or
+    the reference's ``inv_normal`` (invNormalCdf) over an array."""
+    import numpy as np
+    code = {"exp": 0, "log": 1, "erfc": 2, "inv_normal": 3}[fn]
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    err = _native.ErrorC()
+    rc = _native.lib().cltk_debug_math(int(device), code, x.ctypes.data, len(x), out.ctypes.data,
+                                       C.byref(err))
+    _raise(rc, err)
+    return out
 
 
 def fp64_peak(device: int = -1, iters: int = 4096) -> tuple[float, float]:

@@ -17,7 +17,7 @@ EXPORTS = [
     "cltk_version", "cltk_gpu_price", "cltk_gpu_price_batch", "cltk_plan_create",
     "cltk_plan_destroy", "cltk_plan_get_info", "cltk_plan_chunking", "cltk_plan_launch",
     "cltk_plan_finalize", "cltk_plan_error_word", "cltk_plan_set_error_word",
-    "cltk_compile_listing", "cltk_plan_dump", "cltk_free", "cltk_debug_paths", "cltk_debug_rng",
+    "cltk_compile_listing", "cltk_plan_dump", "cltk_free", "cltk_debug_paths", "cltk_debug_rng", "cltk_debug_math",
     "cltk_fp64_peak", "cltk_black_scholes_call",
 ]
 
@@ -87,6 +87,8 @@ def lib() -> C.CDLL:
     L.cltk_debug_paths.argtypes = [vp, u64, u64, u64, vp, vp, vp, P64, PE]
     L.cltk_debug_rng.restype = i32
     L.cltk_debug_rng.argtypes = [i32, u64, u64, u64, u64, vp, vp, vp, PE]
+    L.cltk_debug_math.restype = i32
+    L.cltk_debug_math.argtypes = [i32, i32, vp, u64, vp, PE]
     L.cltk_fp64_peak.restype = i32
     L.cltk_fp64_peak.argtypes = [i32, i32, PD, PD, PE]
     L.cltk_black_scholes_call.restype = dbl

@@ -179,6 +179,11 @@ int cltk_debug_rng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64
   return guarded(err, [&] { debugRng(device, seed, path, i0, n, bits, uniforms, normals); });
 }
 
+int cltk_debug_math(int device, int fn, const double* x, uint64_t n, double* out,
+                    cltk_error* err) {
+  return guarded(err, [&] { debugMath(device, fn, x, n, out); });
+}
+
 int cltk_fp64_peak(int device, int iters, double* tflops, double* seconds, cltk_error* err) {
   return guarded(err, [&] { *tflops = fp64Peak(device, iters, seconds); });
 }

@@ -181,6 +181,8 @@ uint64_t debugPaths(Plan& plan, uint64_t seed, uint64_t path0, uint64_t npaths, 
 void debugRng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n, uint64_t* bits,
               double* uniforms, double* normals);
 double fp64Peak(int device, int iters, double* seconds);
+// Device exp / log / erfc / invNormalCdf (fn 0..3) over a host array.
+void debugMath(int device, int fn, const double* x, uint64_t n, double* out);
 
 // ---- the reference pricing API (proj/include/cltk/pricing.hpp:84-98) --------
 PriceResult priceMC(const Kernel& k, const ModelSpec& model, uint64_t paths, uint64_t seed,

@@ -302,6 +302,19 @@ void debugRng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
   cudaFree(dN);
 }
 
+void debugMath(int device, int fn, const double* x, uint64_t n, double* out) {
+  if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+  double *dx = nullptr, *dy = nullptr;
+  ck(cudaMalloc(&dx, n * sizeof(double)), "cudaMalloc");
+  ck(cudaMalloc(&dy, n * sizeof(double)), "cudaMalloc");
+  ck(cudaMemcpy(dx, x, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+  ck(launchMath(fn, dx, n, dy, nullptr), "math launch");
+  ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  ck(cudaMemcpy(out, dy, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(dx);
+  cudaFree(dy);
+}
+
 double fp64Peak(int device, int iters, double* seconds) {
   if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
   int dev = 0, sms = 0;

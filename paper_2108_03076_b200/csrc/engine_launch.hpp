@@ -53,6 +53,7 @@ cudaError_t launchCombine(const cltk_partial* parts, uint64_t nChunks, uint32_t 
 cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s);
 cudaError_t launchRngDump(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
                           uint64_t* bits, double* uniform, double* normal, cudaStream_t s);
+cudaError_t launchMath(int fn, const double* x, uint64_t n, double* out, cudaStream_t s);
 cudaError_t launchFp64Peak(double* sink, int iters, int grid, cudaStream_t s);
 
 }  // namespace b200

@@ -12,12 +12,14 @@
 // FP64 arithmetic that the reference performs unfused is written with
 // __dadd_rn/__dmul_rn (never contracted into DFMA) and the file is compiled
 // with -fmad=false, so every operation rounds exactly as the x86-64 reference
-// does; exp/log/erfc are the CUDA libdevice routines (a few ulp from glibc).
+// does; exp/log/erfc are glibc's own algorithms (glibc_math.h), so normals
+// and spots are the reference's bit for bit.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
 #include "engine_launch.hpp"
+#include "glibc_math.h"
 #include "program.h"
 
 namespace cltk {
@@ -87,14 +89,14 @@ __device__ __forceinline__ double inv_normal(double p) {
     x = __ddiv_rn(M_(num, q), den);
   } else {
     bool lower = p < K[21];
-    double q = __dsqrt_rn(M_(K[28], log(lower ? p : A_(K[27], -p))));
+    double q = __dsqrt_rn(M_(K[28], cltk_gm::log(lower ? p : A_(K[27], -p))));
     double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[11], q), K[12]), q), K[13]), q), K[14]), q), K[15]), q), K[16]);
     double den = A_(M_(A_(M_(A_(M_(A_(M_(K[17], q), K[18]), q), K[19]), q), K[20]), q), K[27]);
     x = __ddiv_rn(lower ? num : -num, den);
   }
   // Halley step: e = 0.5*erfc(-x/sqrt(2)) - p; u = e*sqrt(2*pi)*exp(x*x/2)
-  double e = A_(M_(K[25], erfc(__ddiv_rn(-x, K[23]))), -p);
-  double u = M_(M_(e, K[24]), exp(M_(M_(x, x), K[25])));
+  double e = A_(M_(K[25], cltk_gm::erfc(__ddiv_rn(-x, K[23]))), -p);
+  double u = M_(M_(e, K[24]), cltk_gm::exp(M_(M_(x, x), K[25])));
   return A_(x, -__ddiv_rn(u, A_(K[27], M_(M_(x, u), K[25]))));
 }
 
@@ -206,7 +208,7 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, uint64
 #pragma unroll
         for (int l = 0; l <= j; ++l) acc = __dadd_rn(acc, __dmul_rn(L[j][l], raw[l]));
         logS[j] = __dadd_rn(logS[j], __dadd_rn(__ldg(&st->A[j]), __dmul_rn(__ldg(&st->B[j]), acc)));
-        S[j] = ((used >> j) & 1u) ? exp(logS[j]) : 0.0;
+        S[j] = ((used >> j) & 1u) ? cltk_gm::exp(logS[j]) : 0.0;
         if (DUMP && dumpZ) dumpZ[s * NA + j] = raw[j];
       }
     } else if (kind == 0) {
@@ -214,7 +216,7 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, uint64
       for (int j = 0; j < NA; ++j) S[j] = __ldg(&st->S[j]);
     } else {
 #pragma unroll
-      for (int j = 0; j < NA; ++j) S[j] = ((used >> j) & 1u) ? exp(logS[j]) : 0.0;
+      for (int j = 0; j < NA; ++j) S[j] = ((used >> j) & 1u) ? cltk_gm::exp(logS[j]) : 0.0;
     }
     if (DUMP && dumpS) {
 #pragma unroll
@@ -453,6 +455,15 @@ __global__ void rng_kernel(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n
   if (nor) nor[k] = inv_normal(u);
 }
 
+// Device build of the glibc routines over an array (tests).
+__global__ void math_kernel(int fn, const double* __restrict__ x, uint64_t n, double* out) {
+  const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double v = x[k];
+  out[k] = fn == 0 ? cltk_gm::exp(v) : fn == 1 ? cltk_gm::log(v) : fn == 2 ? cltk_gm::erfc(v)
+                                                                 : inv_normal(v);
+}
+
 // DFMA throughput probe: 8 independent chains per thread.
 __global__ void __launch_bounds__(256) fp64_peak_kernel(double* sink, int iters) {
   double x[8];
@@ -558,6 +569,12 @@ cudaError_t launchRngDump(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
                           double* uniform, double* normal, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((n + 255) / 256);
   rng_kernel<<<grid, 256, 0, s>>>(seed, path, i0, n, bits, uniform, normal);
+  return cudaGetLastError();
+}
+
+cudaError_t launchMath(int fn, const double* x, uint64_t n, double* out, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+  math_kernel<<<grid, 256, 0, s>>>(fn, x, n, out);
   return cudaGetLastError();
 }
 
