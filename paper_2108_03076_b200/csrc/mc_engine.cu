@@ -78,26 +78,46 @@ __constant__ double kAck[32] = {
     0.02425, 0x1.f395810624dd3p-1, 0x1.6a09e667f3bcdp+0, 0x1.40d931ff62705p+1,
     0.5, -0.5, 1.0, -2.0, 0x1.0p-53, 0.0, 0.0};
 
-__device__ __forceinline__ double inv_normal(double p) {
+__device__ __forceinline__ bool acklam_is_central(double p) {
+  return p >= kAck[21] && p <= kAck[22];
+}
+
+// Central rational (p in [plow, 1 - plow]).
+__device__ __forceinline__ double acklam_central(double p) {
   const double* K = kAck;
-  double x;
-  if (p >= K[21] && p <= K[22]) {
-    double q = A_(p, K[26]);
-    double r = M_(q, q);
-    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[0], r), K[1]), r), K[2]), r), K[3]), r), K[4]), r), K[5]);
-    double den = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[6], r), K[7]), r), K[8]), r), K[9]), r), K[10]), r), K[27]);
-    x = __ddiv_rn(M_(num, q), den);
-  } else {
-    bool lower = p < K[21];
-    double q = __dsqrt_rn(M_(K[28], cltk_gm::log(lower ? p : A_(K[27], -p))));
-    double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[11], q), K[12]), q), K[13]), q), K[14]), q), K[15]), q), K[16]);
-    double den = A_(M_(A_(M_(A_(M_(A_(M_(K[17], q), K[18]), q), K[19]), q), K[20]), q), K[27]);
-    x = __ddiv_rn(lower ? num : -num, den);
-  }
-  // Halley step: e = 0.5*erfc(-x/sqrt(2)) - p; u = e*sqrt(2*pi)*exp(x*x/2)
-  double e = A_(M_(K[25], cltk_gm::erfc(__ddiv_rn(-x, K[23]))), -p);
-  double u = M_(M_(e, K[24]), cltk_gm::exp(M_(M_(x, x), K[25])));
+  const double q = A_(p, K[26]);
+  const double r = M_(q, q);
+  const double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[0], r), K[1]), r), K[2]), r), K[3]), r), K[4]), r), K[5]);
+  const double den = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[6], r), K[7]), r), K[8]), r), K[9]), r), K[10]), r), K[27]);
+  return __ddiv_rn(M_(num, q), den);
+}
+
+// Tail rational (p < plow or p > 1 - plow).
+__device__ __forceinline__ double acklam_tail(double p) {
+  const double* K = kAck;
+  const bool lower = p < K[21];
+  const double q = __dsqrt_rn(M_(K[28], cltk_gm::log(lower ? p : A_(K[27], -p))));
+  const double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[11], q), K[12]), q), K[13]), q), K[14]), q), K[15]), q), K[16]);
+  const double den = A_(M_(A_(M_(A_(M_(A_(M_(K[17], q), K[18]), q), K[19]), q), K[20]), q), K[27]);
+  return __ddiv_rn(lower ? num : -num, den);
+}
+
+// erfc argument of the Halley step: -x / sqrt(2.0)
+__device__ __forceinline__ double halley_arg(double x) { return __ddiv_rn(-x, kAck[23]); }
+
+// Halley step given ef = erfc(-x/sqrt(2)):
+//   e = 0.5*ef - p; u = e*sqrt(2*pi)*exp(x*x/2); x - u/(1 + x*u/2)
+__device__ __forceinline__ double halley(double x, double p, double ef) {
+  const double* K = kAck;
+  const double e = A_(M_(K[25], ef), -p);
+  const double u = M_(M_(e, K[24]), cltk_gm::exp(M_(M_(x, x), K[25])));
   return A_(x, -__ddiv_rn(u, A_(K[27], M_(M_(x, u), K[25]))));
+}
+
+// invNormalCdf for one value (reference and test paths).
+__device__ __forceinline__ double inv_normal(double p) {
+  const double x = acklam_is_central(p) ? acklam_central(p) : acklam_tail(p);
+  return halley(x, p, cltk_gm::erfc(halley_arg(x)));
 }
 
 // ---------------------------------------------------------------------------
@@ -108,6 +128,20 @@ struct Frame {
   const double* C;  // this warp's constant table, pre-offset by -n_thread
   uint32_t nThread;
 };
+
+// Normal-batch scratch (shared memory): per thread kMaxBatch slots of the
+// uniform p, the normal x and the erfc argument/value, register-major
+// ([slot][kBlock]); per warp the lane masks of the rare branches.
+constexpr int kMaxBatch = 12;
+// doubles: X, P, Y slots + the per-warp masks (3 * kMaxBatch u32 per warp)
+constexpr size_t kNormScratchWords = 3 * kMaxBatch * kBlock + (kWarps * 3 * kMaxBatch + 1) / 2;
+struct NormScratch {
+  double* X;
+  double* P;
+  double* Y;
+  uint32_t* mask;  // [3][kMaxBatch] for this warp
+};
+__host__ __device__ constexpr int batchSteps(int na) { return na >= kMaxBatch ? 1 : kMaxBatch / na; }
 
 __device__ __forceinline__ double ld(const Frame f, uint32_t idx) {
   return idx < f.nThread ? f.R[idx * kBlock] : f.C[idx];
@@ -166,15 +200,97 @@ __device__ __noinline__ void run_ops(const Frame f, const uint64_t* __restrict__
   }
 }
 
+// Warp-cooperative compaction: the (slot, lane) items flagged in mask[0..M)
+// are dealt out 32 at a time, so a branch that only a few lanes of a few
+// slots need costs ceil(items / 32) passes instead of one pass per slot.
+template <class F>
+__device__ __forceinline__ void compact_each(const uint32_t* mask, int M, int lane, F f) {
+  int total = 0;
+  for (int m = 0; m < M; ++m) total += __popc(mask[m]);
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    if (k < total) {
+      int m = 0, c = 0;
+      for (;;) {
+        const int n = __popc(mask[m]);
+        if (k < c + n) break;
+        c += n;
+        ++m;
+      }
+      // column of the source lane's thread in the [slot][kBlock] arrays
+      const int src = (threadIdx.x & ~31) + static_cast<int>(__fns(mask[m], 0, k - c + 1));
+      f(m, src);
+    }
+  }
+  __syncwarp();
+}
+
+// M normals of (seed, path), draw indices i0 .. i0+M-1 (bit-exact
+// invNormalCdf(uniform)), into NS.X[m].  Returns false on a domain error
+// (uniform == 1.0) of an index the reference draws: bit (m / na) of
+// stepMask set.
+__device__ __noinline__ bool normals_batch(uint64_t seed, uint64_t path, uint64_t i0, int M,
+                                           int na, uint32_t stepMask, const NormScratch NS) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  bool ok = true;
+  // 1: uniforms; central rational for every lane; tails flagged
+  for (int m = 0; m < M; ++m) {
+    const uint64_t b = philox_bits(seed, i0 + m, path);
+    if ((stepMask >> (m / na)) & 1u) ok = ok && ((b >> 11) != 0x1FFFFFFFFFFFFFULL);
+    const double p = uniform_of(b);
+    const bool central = acklam_is_central(p);
+    NS.P[m * kBlock + tid] = p;
+    NS.X[m * kBlock + tid] = acklam_central(p);
+    const uint32_t tm = __ballot_sync(0xffffffffu, !central);
+    if (lane == 0) NS.mask[m] = tm;
+  }
+  __syncwarp();
+  // 2: tails (~4.9% of draws), compacted
+  compact_each(NS.mask, M, lane, [&](int m, int src) {
+    NS.X[m * kBlock + src] = acklam_tail(NS.P[m * kBlock + src]);
+  });
+  // 3: erfc argument; range |y| < 0.84375 (~77%) for every lane
+  for (int m = 0; m < M; ++m) {
+    const double y = halley_arg(NS.X[m * kBlock + tid]);
+    const int r = cltk_gm::erfc_range(y);
+    const double v = cltk_gm::erfc_r1(y);
+    NS.Y[m * kBlock + tid] = r == cltk_gm::ERFC_R1 ? v : y;
+    const uint32_t m2 = __ballot_sync(0xffffffffu, r == cltk_gm::ERFC_R2);
+    const uint32_t m3 = __ballot_sync(0xffffffffu, r == cltk_gm::ERFC_REST);
+    if (lane == 0) {
+      NS.mask[kMaxBatch + m] = m2;
+      NS.mask[2 * kMaxBatch + m] = m3;
+    }
+  }
+  __syncwarp();
+  // 4: the rarer erfc ranges (~16% and ~8%), compacted
+  compact_each(NS.mask + kMaxBatch, M, lane, [&](int m, int src) {
+    double* y = NS.Y + m * kBlock + src;
+    *y = cltk_gm::erfc_r2(*y);
+  });
+  compact_each(NS.mask + 2 * kMaxBatch, M, lane, [&](int m, int src) {
+    double* y = NS.Y + m * kBlock + src;
+    *y = cltk_gm::erfc_rest(*y);
+  });
+  // 5: Halley step for every lane
+  for (int m = 0; m < M; ++m) {
+    const int o = m * kBlock + tid;
+    NS.X[o] = halley(NS.X[o], NS.P[o], NS.Y[o]);
+  }
+  return ok;
+}
+
 // ---------------------------------------------------------------------------
 // One path: simulate the day grid and run each step's payoff ops.
 // Returns false (and records nothing) on an invNormalCdf domain error; the
 // caller reports it.
 // ---------------------------------------------------------------------------
 template <int NA, bool DUMP>
-__device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, uint64_t seed,
-                                         uint64_t path, double* dumpS, double* dumpZ) {
+__device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const NormScratch NS,
+                                         uint64_t seed, uint64_t path, double* dumpS,
+                                         double* dumpZ) {
   const cltk_plan_header& h = P.hdr;
+  constexpr int SB = batchSteps(NA);
   double logS[NA];
   double L[NA][NA];
 #pragma unroll
@@ -185,31 +301,35 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, uint64
   }
   bool ok = true;
   const uint32_t used = h.used_mask;
+  const int tid = threadIdx.x;
   for (uint32_t s = 0; s < h.n_steps; ++s) {
     const cltk_step* st = P.steps + s;
     const uint32_t kind = __ldg(&st->draws);
+    const uint32_t sb = s % SB;
+    if (sb == 0) {
+      // normals of the next SB steps in one warp-cooperative batch; only the
+      // steps that draw in the reference (dt > 0) count for domain errors
+      const uint32_t nb = min(static_cast<uint32_t>(SB), h.n_steps - s);
+      uint32_t stepMask = 0;
+      for (uint32_t q = 0; q < nb; ++q)
+        if (__ldg(&P.steps[s + q].draws) == 1) stepMask |= 1u << q;
+      // normals of non-drawing steps (day 0) are generated but never used or
+      // checked: the reference draws nothing there
+      if (stepMask)
+        ok = normals_batch(seed, path, static_cast<uint64_t>(s) * NA, static_cast<int>(nb * NA),
+                           NA, stepMask, NS) && ok;
+    }
     double S[NA];
     if (kind == 1) {
-      double raw[NA];
-      // One normal at a time (rolled: keeps the inlined inverse-normal code
-      // once in the I-cache); raw[] stays in registers via the select.
-#pragma unroll 1
-      for (int j = 0; j < NA; ++j) {
-        const uint64_t b = philox_bits(seed, static_cast<uint64_t>(s) * NA + j, path);
-        ok = ok && ((b >> 11) != 0x1FFFFFFFFFFFFFULL);  // uniform() == 1.0
-        const double z = inv_normal(uniform_of(b));
-#pragma unroll
-        for (int q = 0; q < NA; ++q)
-          if (q == j) raw[q] = z;
-      }
 #pragma unroll
       for (int j = 0; j < NA; ++j) {
         double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l <= j; ++l) acc = __dadd_rn(acc, __dmul_rn(L[j][l], raw[l]));
+        for (int l = 0; l <= j; ++l)
+          acc = __dadd_rn(acc, __dmul_rn(L[j][l], NS.X[(sb * NA + l) * kBlock + tid]));
         logS[j] = __dadd_rn(logS[j], __dadd_rn(__ldg(&st->A[j]), __dmul_rn(__ldg(&st->B[j]), acc)));
         S[j] = ((used >> j) & 1u) ? cltk_gm::exp(logS[j]) : 0.0;
-        if (DUMP && dumpZ) dumpZ[s * NA + j] = raw[j];
+        if (DUMP && dumpZ) dumpZ[s * NA + j] = NS.X[(sb * NA + j) * kBlock + tid];
       }
     } else if (kind == 0) {
 #pragma unroll
@@ -279,6 +399,9 @@ __global__ void __launch_bounds__(kBlock) path_kernel(const DevPlan P, const Run
   }
   unsigned long long* chunkSlot =
       reinterpret_cast<unsigned long long*>(counts + kWarps);
+  double* nsBase = reinterpret_cast<double*>(chunkSlot + 1);
+  NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
+                 reinterpret_cast<uint32_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * kMaxBatch};
 
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
@@ -299,7 +422,7 @@ __global__ void __launch_bounds__(kBlock) path_kernel(const DevPlan P, const Run
       const bool active = path < A.paths;
       if (__all_sync(0xffffffffu, !active)) continue;  // warp-uniform
       const uint64_t p = active ? path : A.paths - 1;
-      bool ok = simulate<NA, false>(P, f, A.seed, p, nullptr, nullptr);
+      bool ok = simulate<NA, false>(P, f, NS, A.seed, p, nullptr, nullptr);
       if (active && !ok) atomicMin(A.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
       const uint32_t nAct = __popc(__ballot_sync(0xffffffffu, active));
       const bool first = counts[warp] == 0.0;
@@ -414,12 +537,15 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
   Frame f{smem + tid, wconst - h.n_thread, h.n_thread};
+  double* nsBase = smem + static_cast<size_t>(h.n_thread) * kBlock + kWarps * (nc + ni);
+  NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
+                 reinterpret_cast<uint32_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * kMaxBatch};
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kBlock + tid;
   const bool active = idx < D.npaths;
   const uint64_t q = active ? idx : 0;
   const uint64_t p = D.path0 + q;
   const size_t sz = static_cast<size_t>(h.n_steps) * NA;
-  bool ok = simulate<NA, true>(P, f, D.seed, p, D.spots ? D.spots + q * sz : nullptr,
+  bool ok = simulate<NA, true>(P, f, NS, D.seed, p, D.spots ? D.spots + q * sz : nullptr,
                                D.normals ? D.normals + q * sz : nullptr);
   if (active && !ok) atomicMin(D.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
   for (uint32_t inst = 0; inst < h.n_instances; ++inst) {
@@ -500,7 +626,7 @@ template <int NA>
 cudaError_t launchDumpT(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
   const cltk_plan_header& h = p.hdr;
   size_t smem = (static_cast<size_t>(h.n_thread) * kBlock +
-                 kWarps * (h.n_shared_const + h.n_inst_const)) * sizeof(double);
+                 kWarps * (h.n_shared_const + h.n_inst_const) + kNormScratchWords) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(dump_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024);
   if (e != cudaSuccess) return e;
@@ -529,6 +655,7 @@ size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
   size_t words = static_cast<size_t>(h.n_thread) * kBlock + kWarps * (h.n_shared_const + h.n_inst_const);
   if (accInSmem) words += kWarps * nOut * 3;
   words += kWarps + 1;  // counts + chunk slot
+  words += kNormScratchWords;
   return words * sizeof(double);
 }
 
