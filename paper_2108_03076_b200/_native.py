@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcltk_b200.so")
+LIB_PATH = os.environ.get("CLTK_B200_LIB") or os.path.join(HERE, "libcltk_b200.so")
 
 # Every symbol include/cltk_b200.h declares (tests check the exports).
 EXPORTS = [

@@ -175,6 +175,7 @@ void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void*
   }
   ck(cudaMemsetAsync(I.chunkCounter, 0, sizeof(unsigned long long), s), "cudaMemsetAsync");
   RunArgs a{};
+  a.keys = philoxKeys(seed);
   a.seed = seed;
   a.paths = paths;
   a.chunkPaths = chunkPaths;
@@ -269,7 +270,7 @@ uint64_t debugPaths(Plan& plan, uint64_t seed, uint64_t path0, uint64_t npaths, 
   if (spots && nS) ck(cudaMalloc(&dS, nS * sizeof(double)), "cudaMalloc");
   if (normals && nS) ck(cudaMalloc(&dZ, nS * sizeof(double)), "cudaMalloc");
   if (dZ) ck(cudaMemset(dZ, 0, nS * sizeof(double)), "cudaMemset");
-  DumpArgs a{seed, path0, npaths, dS, dO, dZ, dE};
+  DumpArgs a{philoxKeys(seed), seed, path0, npaths, dS, dO, dZ, dE};
   ck(launchDump(I.dev, a, nullptr), "dump launch");
   ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
   if (dO) ck(cudaMemcpy(outputs, dO, nO * sizeof(double), cudaMemcpyDeviceToHost), "D2H");

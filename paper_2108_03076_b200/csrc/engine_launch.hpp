@@ -11,6 +11,16 @@ namespace b200 {
 constexpr int kBlock = 128;  // threads per CTA (4 warps)
 constexpr int kWarps = kBlock / 32;
 
+// Philox2x64-10 key schedule key_r = seed + r * 0x9E3779B97F4A7C15.
+struct PhiloxKeys {
+  uint64_t k[10];
+};
+inline PhiloxKeys philoxKeys(uint64_t seed) {
+  PhiloxKeys K;
+  for (int r = 0; r < 10; ++r) K.k[r] = seed + static_cast<uint64_t>(r) * 0x9E3779B97F4A7C15ULL;
+  return K;
+}
+
 // Everything the path kernel reads, all device pointers.
 struct DevPlan {
   cltk_plan_header hdr;
@@ -22,6 +32,7 @@ struct DevPlan {
 };
 
 struct RunArgs {
+  PhiloxKeys keys;
   uint64_t seed;
   uint64_t paths;        // total paths of the run (whole job, all GPUs)
   uint64_t chunkPaths;   // kBlock * ppt
@@ -35,6 +46,7 @@ struct RunArgs {
 
 // Dump modes (tests): per-path outputs instead of reduction.
 struct DumpArgs {
+  PhiloxKeys keys;
   uint64_t seed, path0, npaths;
   double* spots;    // [npaths][n_steps][n_assets] or null
   double* outputs;  // [npaths][n_out] or null

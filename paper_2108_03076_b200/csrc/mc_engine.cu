@@ -47,6 +47,20 @@ __device__ __forceinline__ uint64_t philox_bits(uint64_t seed, uint64_t i, uint6
   return c0 ^ c1;
 }
 
+// Same stream with the key schedule key_r = seed + r*W precomputed on the
+// host (kernel parameters: the XOR takes them straight from the constant bank).
+__device__ __forceinline__ uint64_t philox_keyed(const PhiloxKeys& K, uint64_t i, uint64_t path) {
+  uint64_t c0 = i, c1 = path;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t hi = __umul64hi(kPhiloxM, c0);
+    const uint64_t lo = kPhiloxM * c0;
+    c0 = hi ^ K.k[r] ^ c1;
+    c1 = lo;
+  }
+  return c0 ^ c1;
+}
+
 // (double(bits >> 11) + 0.5) * 2^-53  -- exact conversion, one rounding add.
 __device__ __forceinline__ double uniform_of(uint64_t bits) {
   return __dmul_rn(__dadd_rn(__ull2double_rn(bits >> 11), 0.5), 0x1.0p-53);
@@ -132,14 +146,20 @@ struct Frame {
 // Normal-batch scratch (shared memory): per thread kMaxBatch slots of the
 // uniform p, the normal x and the erfc argument/value, register-major
 // ([slot][kBlock]); per warp the lane masks of the rare branches.
-constexpr int kMaxBatch = 12;
-// doubles: X, P, Y slots + the per-warp masks (3 * kMaxBatch u32 per warp)
-constexpr size_t kNormScratchWords = 3 * kMaxBatch * kBlock + (kWarps * 3 * kMaxBatch + 1) / 2;
+#ifndef CLTK_MAX_BATCH
+#define CLTK_MAX_BATCH 12
+#endif
+#ifndef CLTK_MIN_BLOCKS
+#define CLTK_MIN_BLOCKS 1
+#endif
+constexpr int kMaxBatch = CLTK_MAX_BATCH;
+// doubles: X, P, Y slots + the per-warp work lists (3 * 32 * kMaxBatch u16)
+constexpr size_t kNormScratchWords = 3 * kMaxBatch * kBlock + (kWarps * 3 * 32 * kMaxBatch + 3) / 4;
 struct NormScratch {
   double* X;
   double* P;
   double* Y;
-  uint32_t* mask;  // [3][kMaxBatch] for this warp
+  uint16_t* list;  // this warp's 3 work lists of 32 * kMaxBatch (slot, lane) items
 };
 __host__ __device__ constexpr int batchSteps(int na) { return na >= kMaxBatch ? 1 : kMaxBatch / na; }
 
@@ -200,26 +220,26 @@ __device__ __noinline__ void run_ops(const Frame f, const uint64_t* __restrict__
   }
 }
 
-// Warp-cooperative compaction: the (slot, lane) items flagged in mask[0..M)
-// are dealt out 32 at a time, so a branch that only a few lanes of a few
-// slots need costs ceil(items / 32) passes instead of one pass per slot.
+// Warp-cooperative compaction: while a phase walks the slots, every lane
+// that needs a rare branch appends (slot, lane) to a per-warp list in shared
+// memory (ballot + popc prefix); the list is then dealt out 32 items at a
+// time, so a branch that only a few lanes of a few slots need costs
+// ceil(items / 32) passes instead of one pass per slot.
+__device__ __forceinline__ void list_push(uint16_t* list, int& count, bool pred, int m, int lane) {
+  const uint32_t bal = __ballot_sync(0xffffffffu, pred);
+  if (pred) list[count + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>((m << 5) | lane);
+  count += __popc(bal);
+}
+
 template <class F>
-__device__ __forceinline__ void compact_each(const uint32_t* mask, int M, int lane, F f) {
-  int total = 0;
-  for (int m = 0; m < M; ++m) total += __popc(mask[m]);
-  for (int base = 0; base < total; base += 32) {
+__device__ __forceinline__ void list_each(const uint16_t* list, int count, int lane, F f) {
+  __syncwarp();
+  const int wbase = threadIdx.x & ~31;
+  for (int base = 0; base < count; base += 32) {
     const int k = base + lane;
-    if (k < total) {
-      int m = 0, c = 0;
-      for (;;) {
-        const int n = __popc(mask[m]);
-        if (k < c + n) break;
-        c += n;
-        ++m;
-      }
-      // column of the source lane's thread in the [slot][kBlock] arrays
-      const int src = (threadIdx.x & ~31) + static_cast<int>(__fns(mask[m], 0, k - c + 1));
-      f(m, src);
+    if (k < count) {
+      const uint32_t e = list[k];
+      f(static_cast<int>(e >> 5), wbase + static_cast<int>(e & 31u));
     }
   }
   __syncwarp();
@@ -227,67 +247,87 @@ __device__ __forceinline__ void compact_each(const uint32_t* mask, int M, int la
 
 // M normals of (seed, path), draw indices i0 .. i0+M-1 (bit-exact
 // invNormalCdf(uniform)), into NS.X[m].  Returns false on a domain error
-// (uniform == 1.0) of an index the reference draws: bit (m / na) of
-// stepMask set.
-__device__ __noinline__ bool normals_batch(uint64_t seed, uint64_t path, uint64_t i0, int M,
-                                           int na, uint32_t stepMask, const NormScratch NS) {
+// (uniform == 1.0) of an index the reference draws (bit m of drawMask).
+// The per-slot phases walk two slots at a time (independent dependency
+// chains the scheduler interleaves).
+__device__ __forceinline__ bool normals_batch(const PhiloxKeys& K, uint64_t path, uint64_t i0,
+                                              int M, uint32_t drawMask, const NormScratch NS) {
   const int tid = threadIdx.x, lane = tid & 31;
+  uint16_t* tails = NS.list;
+  uint16_t* r2 = NS.list + 32 * kMaxBatch;
+  uint16_t* r3 = NS.list + 64 * kMaxBatch;
+  int nTail = 0, n2 = 0, n3 = 0;
   bool ok = true;
-  // 1: uniforms; central rational for every lane; tails flagged
-  for (int m = 0; m < M; ++m) {
-    const uint64_t b = philox_bits(seed, i0 + m, path);
-    if ((stepMask >> (m / na)) & 1u) ok = ok && ((b >> 11) != 0x1FFFFFFFFFFFFFULL);
+  // 1: uniforms; central rational for every lane; tails listed
+  auto phase1 = [&](int m) {
+    const uint64_t b = philox_keyed(K, i0 + m, path);
     const double p = uniform_of(b);
-    const bool central = acklam_is_central(p);
     NS.P[m * kBlock + tid] = p;
     NS.X[m * kBlock + tid] = acklam_central(p);
-    const uint32_t tm = __ballot_sync(0xffffffffu, !central);
-    if (lane == 0) NS.mask[m] = tm;
+    return b;
+  };
+  int m = 0;
+  for (; m + 1 < M; m += 2) {
+    const uint64_t b0 = phase1(m), b1 = phase1(m + 1);
+    if ((drawMask >> m) & 1u) ok = ok && ((b0 >> 11) != 0x1FFFFFFFFFFFFFULL);
+    if ((drawMask >> (m + 1)) & 1u) ok = ok && ((b1 >> 11) != 0x1FFFFFFFFFFFFFULL);
+    list_push(tails, nTail, !acklam_is_central(NS.P[m * kBlock + tid]), m, lane);
+    list_push(tails, nTail, !acklam_is_central(NS.P[(m + 1) * kBlock + tid]), m + 1, lane);
   }
-  __syncwarp();
-  // 2: tails (~4.9% of draws), compacted
-  compact_each(NS.mask, M, lane, [&](int m, int src) {
-    NS.X[m * kBlock + src] = acklam_tail(NS.P[m * kBlock + src]);
+  if (m < M) {
+    const uint64_t b0 = phase1(m);
+    if ((drawMask >> m) & 1u) ok = ok && ((b0 >> 11) != 0x1FFFFFFFFFFFFFULL);
+    list_push(tails, nTail, !acklam_is_central(NS.P[m * kBlock + tid]), m, lane);
+  }
+  // 2: tails (~4.9% of draws)
+  list_each(tails, nTail, lane, [&](int q, int src) {
+    NS.X[q * kBlock + src] = acklam_tail(NS.P[q * kBlock + src]);
   });
   // 3: erfc argument; range |y| < 0.84375 (~77%) for every lane
-  for (int m = 0; m < M; ++m) {
-    const double y = halley_arg(NS.X[m * kBlock + tid]);
+  auto phase3 = [&](int q) {
+    const double y = halley_arg(NS.X[q * kBlock + tid]);
     const int r = cltk_gm::erfc_range(y);
     const double v = cltk_gm::erfc_r1(y);
-    NS.Y[m * kBlock + tid] = r == cltk_gm::ERFC_R1 ? v : y;
-    const uint32_t m2 = __ballot_sync(0xffffffffu, r == cltk_gm::ERFC_R2);
-    const uint32_t m3 = __ballot_sync(0xffffffffu, r == cltk_gm::ERFC_REST);
-    if (lane == 0) {
-      NS.mask[kMaxBatch + m] = m2;
-      NS.mask[2 * kMaxBatch + m] = m3;
-    }
+    NS.Y[q * kBlock + tid] = r == cltk_gm::ERFC_R1 ? v : y;
+    return r;
+  };
+  for (m = 0; m + 1 < M; m += 2) {
+    const int ra = phase3(m), rb = phase3(m + 1);
+    list_push(r2, n2, ra == cltk_gm::ERFC_R2, m, lane);
+    list_push(r3, n3, ra == cltk_gm::ERFC_REST, m, lane);
+    list_push(r2, n2, rb == cltk_gm::ERFC_R2, m + 1, lane);
+    list_push(r3, n3, rb == cltk_gm::ERFC_REST, m + 1, lane);
   }
-  __syncwarp();
-  // 4: the rarer erfc ranges (~16% and ~8%), compacted
-  compact_each(NS.mask + kMaxBatch, M, lane, [&](int m, int src) {
-    double* y = NS.Y + m * kBlock + src;
+  if (m < M) {
+    const int ra = phase3(m);
+    list_push(r2, n2, ra == cltk_gm::ERFC_R2, m, lane);
+    list_push(r3, n3, ra == cltk_gm::ERFC_REST, m, lane);
+  }
+  // 4: the rarer erfc ranges (~16% and ~8%)
+  list_each(r2, n2, lane, [&](int q, int src) {
+    double* y = NS.Y + q * kBlock + src;
     *y = cltk_gm::erfc_r2(*y);
   });
-  compact_each(NS.mask + 2 * kMaxBatch, M, lane, [&](int m, int src) {
-    double* y = NS.Y + m * kBlock + src;
+  list_each(r3, n3, lane, [&](int q, int src) {
+    double* y = NS.Y + q * kBlock + src;
     *y = cltk_gm::erfc_rest(*y);
   });
   // 5: Halley step for every lane
-  for (int m = 0; m < M; ++m) {
-    const int o = m * kBlock + tid;
+  auto phase5 = [&](int q) {
+    const int o = q * kBlock + tid;
     NS.X[o] = halley(NS.X[o], NS.P[o], NS.Y[o]);
+  };
+  for (m = 0; m + 1 < M; m += 2) {
+    phase5(m);
+    phase5(m + 1);
   }
+  if (m < M) phase5(m);
   return ok;
 }
 
-// ---------------------------------------------------------------------------
-// One path: simulate the day grid and run each step's payoff ops.
-// Returns false (and records nothing) on an invNormalCdf domain error; the
-// caller reports it.
-// ---------------------------------------------------------------------------
 template <int NA, bool DUMP>
 __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const NormScratch NS,
-                                         uint64_t seed, uint64_t path, double* dumpS,
+                                         const PhiloxKeys& keys, uint64_t path, double* dumpS,
                                          double* dumpZ) {
   const cltk_plan_header& h = P.hdr;
   constexpr int SB = batchSteps(NA);
@@ -310,14 +350,14 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const 
       // normals of the next SB steps in one warp-cooperative batch; only the
       // steps that draw in the reference (dt > 0) count for domain errors
       const uint32_t nb = min(static_cast<uint32_t>(SB), h.n_steps - s);
-      uint32_t stepMask = 0;
+      uint32_t drawMask = 0;
       for (uint32_t q = 0; q < nb; ++q)
-        if (__ldg(&P.steps[s + q].draws) == 1) stepMask |= 1u << q;
+        if (__ldg(&P.steps[s + q].draws) == 1) drawMask |= ((1u << NA) - 1u) << (q * NA);
       // normals of non-drawing steps (day 0) are generated but never used or
       // checked: the reference draws nothing there
-      if (stepMask)
-        ok = normals_batch(seed, path, static_cast<uint64_t>(s) * NA, static_cast<int>(nb * NA),
-                           NA, stepMask, NS) && ok;
+      if (drawMask)
+        ok = normals_batch(keys, path, static_cast<uint64_t>(s) * NA, static_cast<int>(nb * NA),
+                           drawMask, NS) && ok;
     }
     double S[NA];
     if (kind == 1) {
@@ -377,7 +417,7 @@ __device__ __forceinline__ void chan(double& n, double& mean, double& m2, double
 
 // Shared memory: [regs n_thread*kBlock][wconst kWarps*(nc+ni)][acc ...][misc]
 template <int NA>
-__global__ void __launch_bounds__(kBlock) path_kernel(const DevPlan P, const RunArgs A,
+__global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const DevPlan P, const RunArgs A,
                                                       int accInSmem) {
   extern __shared__ double smem[];
   const cltk_plan_header& h = P.hdr;
@@ -401,7 +441,7 @@ __global__ void __launch_bounds__(kBlock) path_kernel(const DevPlan P, const Run
       reinterpret_cast<unsigned long long*>(counts + kWarps);
   double* nsBase = reinterpret_cast<double*>(chunkSlot + 1);
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
-                 reinterpret_cast<uint32_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * kMaxBatch};
+                 reinterpret_cast<uint16_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * 32 * kMaxBatch};
 
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
@@ -422,7 +462,7 @@ __global__ void __launch_bounds__(kBlock) path_kernel(const DevPlan P, const Run
       const bool active = path < A.paths;
       if (__all_sync(0xffffffffu, !active)) continue;  // warp-uniform
       const uint64_t p = active ? path : A.paths - 1;
-      bool ok = simulate<NA, false>(P, f, NS, A.seed, p, nullptr, nullptr);
+      bool ok = simulate<NA, false>(P, f, NS, A.keys, p, nullptr, nullptr);
       if (active && !ok) atomicMin(A.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
       const uint32_t nAct = __popc(__ballot_sync(0xffffffffu, active));
       const bool first = counts[warp] == 0.0;
@@ -539,13 +579,13 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
   Frame f{smem + tid, wconst - h.n_thread, h.n_thread};
   double* nsBase = smem + static_cast<size_t>(h.n_thread) * kBlock + kWarps * (nc + ni);
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
-                 reinterpret_cast<uint32_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * kMaxBatch};
+                 reinterpret_cast<uint16_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * 32 * kMaxBatch};
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kBlock + tid;
   const bool active = idx < D.npaths;
   const uint64_t q = active ? idx : 0;
   const uint64_t p = D.path0 + q;
   const size_t sz = static_cast<size_t>(h.n_steps) * NA;
-  bool ok = simulate<NA, true>(P, f, NS, D.seed, p, D.spots ? D.spots + q * sz : nullptr,
+  bool ok = simulate<NA, true>(P, f, NS, D.keys, p, D.spots ? D.spots + q * sz : nullptr,
                                D.normals ? D.normals + q * sz : nullptr);
   if (active && !ok) atomicMin(D.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
   for (uint32_t inst = 0; inst < h.n_instances; ++inst) {
