@@ -137,20 +137,35 @@ __device__ __forceinline__ double inv_normal(double p) {
 // ---------------------------------------------------------------------------
 // Payoff program interpreter (operand space: program.h).
 // ---------------------------------------------------------------------------
+// Interpreter frame, as 32-bit shared-memory addresses (LDS/STS, no
+// generic-address translation): operand r < n_thread lives at
+// R + r * kBlock * 8, a constant operand r at C + r * 8.
 struct Frame {
-  double* R;        // this thread's register column: operand r at R[r * kBlock]
-  const double* C;  // this warp's constant table, pre-offset by -n_thread
+  uint32_t R;        // this thread's register column
+  uint32_t C;        // this warp's constant table, pre-offset by -n_thread * 8
   uint32_t nThread;
 };
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 
 // Normal-batch scratch (shared memory): per thread kMaxBatch slots of the
 // uniform p, the normal x and the erfc argument/value, register-major
 // ([slot][kBlock]); per warp the lane masks of the rare branches.
 #ifndef CLTK_MAX_BATCH
-#define CLTK_MAX_BATCH 12
+#define CLTK_MAX_BATCH 6
 #endif
 #ifndef CLTK_MIN_BLOCKS
-#define CLTK_MIN_BLOCKS 1
+#define CLTK_MIN_BLOCKS 5
 #endif
 constexpr int kMaxBatch = CLTK_MAX_BATCH;
 // doubles: X, P, Y slots + the per-warp work lists (3 * 32 * kMaxBatch u16)
@@ -164,7 +179,10 @@ struct NormScratch {
 __host__ __device__ constexpr int batchSteps(int na) { return na >= kMaxBatch ? 1 : kMaxBatch / na; }
 
 __device__ __forceinline__ double ld(const Frame f, uint32_t idx) {
-  return idx < f.nThread ? f.R[idx * kBlock] : f.C[idx];
+  return lds64(idx < f.nThread ? f.R + idx * (kBlock * 8) : f.C + idx * 8);
+}
+__device__ __forceinline__ void st_reg(const Frame f, uint32_t idx, double v) {
+  sts64(f.R + idx * (kBlock * 8), v);
 }
 
 __device__ __forceinline__ int64_t bits_of(double v) { return __double_as_longlong(v); }
@@ -179,44 +197,49 @@ __device__ __noinline__ void run_ops(const Frame f, const uint64_t* __restrict__
     const double va = ld(f, static_cast<uint32_t>(w >> 22) & 0x3fff);
     const double vb = ld(f, static_cast<uint32_t>(w >> 36) & 0x3fff);
     double r;
-    switch (op) {
-      case OP_MOV: r = va; break;
-      case OP_NEG: r = -va; break;
-      case OP_NOT: r = va == 0.0 ? 1.0 : 0.0; break;
-      case OP_ADD: r = __dadd_rn(va, vb); break;
-      case OP_SUB: r = __dsub_rn(va, vb); break;
-      case OP_MUL: r = __dmul_rn(va, vb); break;
-      case OP_DIV: r = __ddiv_rn(va, vb); break;
-      case OP_LT: r = va < vb ? 1.0 : 0.0; break;
-      case OP_LEQ: r = va <= vb ? 1.0 : 0.0; break;
-      case OP_EQ: r = va == vb ? 1.0 : 0.0; break;
-      case OP_AND: r = (va != 0.0 && vb != 0.0) ? 1.0 : 0.0; break;
-      case OP_OR: r = (va != 0.0 || vb != 0.0) ? 1.0 : 0.0; break;
-      case OP_SEL: r = va != 0.0 ? vb : ld(f, static_cast<uint32_t>(w >> 50) & 0x3fff); break;
-      case OP_IADD:
-        r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) +
-                                         static_cast<uint64_t>(bits_of(vb))));
-        break;
-      case OP_ISUB:
-        r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) -
-                                         static_cast<uint64_t>(bits_of(vb))));
-        break;
-      case OP_ILT: r = bits_of(va) < bits_of(vb) ? 1.0 : 0.0; break;
-      case OP_ILEQ: r = bits_of(va) <= bits_of(vb) ? 1.0 : 0.0; break;
-      case OP_IEQ: r = bits_of(va) == bits_of(vb) ? 1.0 : 0.0; break;
-      case OP_MIN: r = fmin(va, vb); break;
-      case OP_MAX: r = fmax(va, vb); break;
-      case OP_MINP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                 : fmin(va, vb);
-        break;
-      case OP_MAXP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                 : fmax(va, vb);
-        break;
-      case OP_EFIRST: r = bits_of(va) != 0 ? va : vb; break;
-      case OP_EDIVZ: r = va == 0.0 ? of_bits(static_cast<int64_t>(w >> 50)) : 0.0; break;
-      default: r = 0.0; break;
+    // the running min/max of barrier monitoring first, then the rest
+    if (op == OP_MIN) {
+      r = fmin(va, vb);
+    } else if (op == OP_MAX) {
+      r = fmax(va, vb);
+    } else {
+      switch (op) {
+        case OP_MOV: r = va; break;
+        case OP_NEG: r = -va; break;
+        case OP_NOT: r = va == 0.0 ? 1.0 : 0.0; break;
+        case OP_ADD: r = __dadd_rn(va, vb); break;
+        case OP_SUB: r = __dsub_rn(va, vb); break;
+        case OP_MUL: r = __dmul_rn(va, vb); break;
+        case OP_DIV: r = __ddiv_rn(va, vb); break;
+        case OP_LT: r = va < vb ? 1.0 : 0.0; break;
+        case OP_LEQ: r = va <= vb ? 1.0 : 0.0; break;
+        case OP_EQ: r = va == vb ? 1.0 : 0.0; break;
+        case OP_AND: r = (va != 0.0 && vb != 0.0) ? 1.0 : 0.0; break;
+        case OP_OR: r = (va != 0.0 || vb != 0.0) ? 1.0 : 0.0; break;
+        case OP_SEL: r = va != 0.0 ? vb : ld(f, static_cast<uint32_t>(w >> 50) & 0x3fff); break;
+        case OP_IADD:
+          r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) +
+                                           static_cast<uint64_t>(bits_of(vb))));
+          break;
+        case OP_ISUB:
+          r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) -
+                                           static_cast<uint64_t>(bits_of(vb))));
+          break;
+        case OP_ILT: r = bits_of(va) < bits_of(vb) ? 1.0 : 0.0; break;
+        case OP_ILEQ: r = bits_of(va) <= bits_of(vb) ? 1.0 : 0.0; break;
+        case OP_IEQ: r = bits_of(va) == bits_of(vb) ? 1.0 : 0.0; break;
+        case OP_MINP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                   : fmin(va, vb);
+          break;
+        case OP_MAXP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                   : fmax(va, vb);
+          break;
+        case OP_EFIRST: r = bits_of(va) != 0 ? va : vb; break;
+        case OP_EDIVZ: r = va == 0.0 ? of_bits(static_cast<int64_t>(w >> 50)) : 0.0; break;
+        default: r = 0.0; break;
+      }
     }
-    f.R[d * kBlock] = r;
+    st_reg(f, d, r);
   }
 }
 
@@ -331,14 +354,11 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const 
                                          double* dumpZ) {
   const cltk_plan_header& h = P.hdr;
   constexpr int SB = batchSteps(NA);
+  // the Cholesky factor is read straight from the kernel-parameter bank at
+  // each use (uniform c[] operands, no registers held across the batch)
   double logS[NA];
-  double L[NA][NA];
 #pragma unroll
-  for (int j = 0; j < NA; ++j) {
-    logS[j] = h.logS0[j];
-#pragma unroll
-    for (int l = 0; l < NA; ++l) L[j][l] = h.chol[j * CLTK_MAX_ASSETS + l];
-  }
+  for (int j = 0; j < NA; ++j) logS[j] = h.logS0[j];
   bool ok = true;
   const uint32_t used = h.used_mask;
   const int tid = threadIdx.x;
@@ -366,7 +386,7 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const 
         double acc = 0.0;
 #pragma unroll
         for (int l = 0; l <= j; ++l)
-          acc = __dadd_rn(acc, __dmul_rn(L[j][l], NS.X[(sb * NA + l) * kBlock + tid]));
+          acc = __dadd_rn(acc, __dmul_rn(h.chol[j * CLTK_MAX_ASSETS + l], NS.X[(sb * NA + l) * kBlock + tid]));
         logS[j] = __dadd_rn(logS[j], __dadd_rn(__ldg(&st->A[j]), __dmul_rn(__ldg(&st->B[j]), acc)));
         S[j] = ((used >> j) & 1u) ? cltk_gm::exp(logS[j]) : 0.0;
         if (DUMP && dumpZ) dumpZ[s * NA + j] = NS.X[(sb * NA + j) * kBlock + tid];
@@ -385,7 +405,7 @@ __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const 
     const uint32_t cb = __ldg(&st->code_begin), ce = __ldg(&st->code_end);
     if (cb < ce) {
 #pragma unroll
-      for (int j = 0; j < NA; ++j) f.R[j * kBlock] = S[j];
+      for (int j = 0; j < NA; ++j) st_reg(f, j, S[j]);
       run_ops(f, P.code, cb, ce);
     }
   }
@@ -445,7 +465,7 @@ __global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const Dev
 
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
-  Frame f{regs + tid, wconst - h.n_thread, h.n_thread};
+  Frame f{smem_addr(regs + tid), smem_addr(wconst) - h.n_thread * 8u, h.n_thread};
 
   for (;;) {
     if (tid == 0) *chunkSlot = A.c0 + atomicAdd(A.chunkCounter, 1ULL);
@@ -576,7 +596,7 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
   double* wconst = smem + static_cast<size_t>(h.n_thread) * kBlock + warp * (nc + ni);
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
-  Frame f{smem + tid, wconst - h.n_thread, h.n_thread};
+  Frame f{smem_addr(smem + tid), smem_addr(wconst) - h.n_thread * 8u, h.n_thread};
   double* nsBase = smem + static_cast<size_t>(h.n_thread) * kBlock + kWarps * (nc + ni);
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
                  reinterpret_cast<uint16_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * 32 * kMaxBatch};
