@@ -24,7 +24,32 @@ from . import Kernel, Plan
 
 
 def shard(n_chunks: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous chunk range of ``rank``: the ranges tile [0, n_chunks)."""
     return n_chunks * rank // world, n_chunks * (rank + 1) // world
+
+
+_SIGN = -(2**63)
+
+
+def merge_partials_(parts: torch.Tensor, group=None) -> torch.Tensor:
+    """The single data-path collective: every element of the full-size
+    partials buffer has exactly one non-zero contributor (its chunk's owner),
+    so the SUM all-reduce reproduces it exactly on every rank."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=group)
+    return parts
+
+
+def merge_error_word(word: int, device: torch.device | str = "cpu", group=None) -> int:
+    """MIN over ranks of the unsigned device error words (path << 24 | site;
+    2^64-1 = no error): the lowest failing path wins on every rank, as it
+    would in a single-GPU run."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return word
+    signed = (word & (2**64 - 1)) - 2**64 if word >= 2**63 else word
+    t = torch.tensor([signed ^ _SIGN], dtype=torch.int64, device=device)  # order-preserving
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return (int(t.item()) ^ _SIGN) & (2**64 - 1)
 
 
 class DistributedPricer:
@@ -57,20 +82,13 @@ class DistributedPricer:
         c0, c1 = shard(nc, self.rank, self.world)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self.plan.launch(paths, seed, c0, c1, parts.data_ptr(), stream)
-        if self.world > 1:
-            dist.all_reduce(parts, op=dist.ReduceOp.SUM)
-        return parts
+        return merge_partials_(parts)
 
     def finalize(self, paths: int, seed: int, parts: torch.Tensor) -> list[dict]:
         stream = torch.cuda.current_stream(self.device).cuda_stream
         if self.world > 1:
-            word = torch.tensor([self.plan.error_word(stream)], dtype=torch.int64,
-                                device=f"cuda:{self.device}")
-            # error words are unsigned; flip the sign bit so signed MIN orders them
-            word ^= torch.tensor([-(2**63)], dtype=torch.int64, device=word.device)
-            dist.all_reduce(word, op=dist.ReduceOp.MIN)
-            w = int(word.item()) ^ -(2**63)
-            self.plan.set_error_word(w & (2**64 - 1), stream)
+            w = merge_error_word(self.plan.error_word(stream), f"cuda:{self.device}")
+            self.plan.set_error_word(w, stream)
         return self.plan.finalize(paths, seed, parts.data_ptr(), stream)
 
     def price(self, paths: int, seed: int) -> list[dict]:
