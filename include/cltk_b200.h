@@ -80,7 +80,26 @@ int cltk_gpu_price_batch(const char* const* kernel_jsons, size_t n_instances,
                          const uint64_t* days, size_t n_days, const char* tenv_json, int device,
                          cltk_price_result* results, cltk_error* err);
 
+/* Template batch as "template parameters passed as kernel arguments": one
+ * kernel and literals[n_instances][n_literals], the values of its float
+ * literals (FloatLit nodes, postorder of the kernel JSON tree -- the order
+ * cltk_kernel_literals returns) for each instance.  One compile, one path
+ * set; results[n_instances * n_days], instance-major. */
+int cltk_gpu_price_template(const char* kernel_json, const double* literals, size_t n_instances,
+                            size_t n_literals, const char* model_json, uint64_t paths,
+                            uint64_t seed, const uint64_t* days, size_t n_days,
+                            const char* tenv_json, int device, cltk_price_result* results,
+                            cltk_error* err);
+/* Host-only: the kernel's float literals in the order above (*n = count;
+ * at most cap values written). */
+int cltk_kernel_literals(const char* kernel_json, double* out, size_t cap, size_t* n,
+                         cltk_error* err);
+
 /* ---- plan API: compile once, launch chunk ranges, combine --------------- */
+int cltk_plan_create_template(const char* kernel_json, const double* literals, size_t n_instances,
+                              size_t n_literals, const char* model_json, const uint64_t* days,
+                              size_t n_days, const char* tenv_json, int device, int rewrite,
+                              cltk_plan** plan, cltk_error* err);
 int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const char* model_json,
                      const uint64_t* days, size_t n_days, const char* tenv_json, int device,
                      int rewrite, cltk_plan** plan, cltk_error* err);

@@ -36,6 +36,7 @@ __all__ = [
     "Kernel", "ContractError", "ContractParseError", "ContractTypeError",
     "ContractUnsupportedError", "price", "price_batch", "black_scholes_call", "Plan",
     "compile_listing", "debug_rng", "debug_math", "fp64_peak", "load_kernel", "version",
+    "kernel_literals", "price_template",
 ]
 
 
@@ -223,6 +224,42 @@ def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths
     return [flat[i * nd:(i + 1) * nd] for i in range(n)]
 
 
+def kernel_literals(kernel: Kernel | str | dict) -> list[float]:
+    """The kernel's float literals in the engine's template order (host only)."""
+    import numpy as np
+    L = _native.lib()
+    kj = _kernel_json(kernel)
+    n = C.c_size_t()
+    err = _native.ErrorC()
+    _raise(L.cltk_kernel_literals(kj, None, 0, C.byref(n), C.byref(err)), err)
+    out = np.zeros(max(1, n.value))
+    _raise(L.cltk_kernel_literals(kj, out.ctypes.data, n.value, C.byref(n), C.byref(err)), err)
+    return [float(x) for x in out[:n.value]]
+
+
+def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
+                   paths: int = 100000, seed: int = 0, days: Sequence[int] = (0,),
+                   tenv: dict | None = None, device: int = -1) -> list[list[dict]]:
+    """Price instances of one template given as a literal table
+    ``literals[instance][j]`` (j in ``kernel_literals`` order): one compile,
+    one path set, the literals passed to the kernel as data."""
+    import numpy as np
+    lit = np.ascontiguousarray(literals, dtype=np.float64)
+    if lit.ndim != 2:
+        raise ValueError("literals must be [n_instances][n_literals]")
+    L = _native.lib()
+    d, nd = _days(days)
+    n = lit.shape[0]
+    out = (_native.PriceResultC * max(1, n * nd))()
+    err = _native.ErrorC()
+    rc = L.cltk_gpu_price_template(_kernel_json(kernel), lit.ctypes.data, n, lit.shape[1],
+                                   _model_json(model), int(paths), int(seed), d, nd,
+                                   _tenv_json(tenv), int(device), out, C.byref(err))
+    _raise(rc, err)
+    flat = _results(out, n * nd)
+    return [flat[i * nd:(i + 1) * nd] for i in range(n)]
+
+
 def black_scholes_call(spot: float, strike: float, rate: float, vol: float,
                        expiry: float) -> float:
     return _native.lib().cltk_black_scholes_call(spot, strike, rate, vol, expiry)
@@ -253,18 +290,26 @@ class Plan:
 
     def __init__(self, kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
                  days: Sequence[int] = (0,), tenv: dict | None = None, device: int = -1,
-                 rewrite: bool = True):
+                 rewrite: bool = True, literals=None):
         if not isinstance(kernels, (list, tuple)):
             kernels = [kernels]
         self._L = _native.lib()
         self.days = [int(x) for x in days]
         d, nd = _days(self.days)
-        arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
         self._h = C.c_void_p()
         err = _native.ErrorC()
-        rc = self._L.cltk_plan_create(arr, len(kernels), _model_json(model), d, nd,
-                                      _tenv_json(tenv), int(device), int(rewrite),
-                                      C.byref(self._h), C.byref(err))
+        if literals is not None:
+            import numpy as np
+            lit = np.ascontiguousarray(literals, dtype=np.float64)
+            rc = self._L.cltk_plan_create_template(
+                _kernel_json(kernels[0]), lit.ctypes.data, lit.shape[0], lit.shape[1],
+                _model_json(model), d, nd, _tenv_json(tenv), int(device), int(rewrite),
+                C.byref(self._h), C.byref(err))
+        else:
+            arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
+            rc = self._L.cltk_plan_create(arr, len(kernels), _model_json(model), d, nd,
+                                          _tenv_json(tenv), int(device), int(rewrite),
+                                          C.byref(self._h), C.byref(err))
         _raise(rc, err)
         info = _native.PlanInfoC()
         self._L.cltk_plan_get_info(self._h, C.byref(info))

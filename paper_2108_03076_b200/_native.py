@@ -18,7 +18,8 @@ EXPORTS = [
     "cltk_plan_destroy", "cltk_plan_get_info", "cltk_plan_chunking", "cltk_plan_launch",
     "cltk_plan_finalize", "cltk_plan_error_word", "cltk_plan_set_error_word",
     "cltk_compile_listing", "cltk_plan_dump", "cltk_free", "cltk_debug_paths", "cltk_debug_rng", "cltk_debug_math",
-    "cltk_fp64_peak", "cltk_black_scholes_call",
+    "cltk_fp64_peak", "cltk_black_scholes_call", "cltk_gpu_price_template",
+    "cltk_kernel_literals", "cltk_plan_create_template",
 ]
 
 
@@ -61,6 +62,14 @@ def lib() -> C.CDLL:
     L.cltk_gpu_price_batch.restype = i32
     L.cltk_gpu_price_batch.argtypes = [C.POINTER(cp), C.c_size_t, cp, u64, u64, P64, C.c_size_t,
                                        cp, i32, PR, PE]
+    L.cltk_gpu_price_template.restype = i32
+    L.cltk_gpu_price_template.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, u64, u64, P64,
+                                          C.c_size_t, cp, i32, PR, PE]
+    L.cltk_kernel_literals.restype = i32
+    L.cltk_kernel_literals.argtypes = [cp, vp, C.c_size_t, C.POINTER(C.c_size_t), PE]
+    L.cltk_plan_create_template.restype = i32
+    L.cltk_plan_create_template.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t,
+                                            cp, i32, i32, C.POINTER(vp), PE]
     L.cltk_plan_create.restype = i32
     L.cltk_plan_create.argtypes = [C.POINTER(cp), C.c_size_t, cp, P64, C.c_size_t, cp, i32, i32,
                                    C.POINTER(vp), PE]

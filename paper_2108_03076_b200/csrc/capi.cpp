@@ -104,6 +104,50 @@ int cltk_gpu_price_batch(const char* const* kernel_jsons, size_t n_instances,
   });
 }
 
+int cltk_gpu_price_template(const char* kernel_json, const double* literals, size_t n_instances,
+                            size_t n_literals, const char* model_json, uint64_t paths,
+                            uint64_t seed, const uint64_t* days, size_t n_days,
+                            const char* tenv_json, int device, cltk_price_result* results,
+                            cltk_error* err) {
+  return guarded(err, [&] {
+    if (paths == 0) throw EvalError("path count must be positive");
+    Kernel k = kernelFromJson(kernel_json);
+    ModelSpec m = modelFromJson(model_json);
+    RunOptions opt;
+    opt.device = device;
+    toC(priceTemplate(k, literals, n_instances, n_literals, m, paths, seed,
+                      std::vector<uint64_t>(days, days + n_days), tenvOf(tenv_json), opt),
+        results);
+  });
+}
+
+int cltk_kernel_literals(const char* kernel_json, double* out, size_t cap, size_t* n,
+                         cltk_error* err) {
+  return guarded(err, [&] {
+    std::vector<double> v = kernelFloatLiterals(kernelFromJson(kernel_json));
+    *n = v.size();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+  });
+}
+
+int cltk_plan_create_template(const char* kernel_json, const double* literals, size_t n_instances,
+                              size_t n_literals, const char* model_json, const uint64_t* days,
+                              size_t n_days, const char* tenv_json, int device, int rewrite,
+                              cltk_plan** out, cltk_error* err) {
+  return guarded(err, [&] {
+    auto p = std::make_unique<cltk_plan>();
+    p->kernels.push_back(std::make_unique<Kernel>(kernelFromJson(kernel_json)));
+    ModelSpec m = modelFromJson(model_json);
+    RunOptions opt;
+    opt.device = device;
+    opt.rewrite = rewrite != 0;
+    p->plan = std::make_unique<Plan>(*p->kernels[0], literals, n_instances, n_literals, m,
+                                     std::vector<uint64_t>(days, days + n_days),
+                                     tenvOf(tenv_json), opt);
+    *out = p.release();
+  });
+}
+
 int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const char* model_json,
                      const uint64_t* days, size_t n_days, const char* tenv_json, int device,
                      int rewrite, cltk_plan** out, cltk_error* err) {

@@ -148,6 +148,12 @@ class Plan {
   // One template (instances[0]) and its literal instances (same shape).
   Plan(const std::vector<const Kernel*>& instances, const ModelSpec& model,
        const std::vector<uint64_t>& days, const TEnv& tenv, const RunOptions& opt);
+  // One template and a literal table: literals[i * nLits + j] is float
+  // literal j (FloatLit nodes in postorder of the kernel JSON tree) of
+  // instance i -- "template parameters passed as kernel arguments".
+  Plan(const Kernel& templ, const double* literals, std::size_t nInstances, std::size_t nLits,
+       const ModelSpec& model, const std::vector<uint64_t>& days, const TEnv& tenv,
+       const RunOptions& opt);
   ~Plan();
   Plan(const Plan&) = delete;
   Plan& operator=(const Plan&) = delete;
@@ -169,6 +175,8 @@ class Plan {
   PlanImpl* impl() { return impl_.get(); }
 
  private:
+  void init(const Kernel& k, const void* lits, const ModelSpec& model,
+            const std::vector<uint64_t>& days, const TEnv& tenv, const RunOptions& opt);
   std::unique_ptr<PlanImpl> impl_;
 };
 
@@ -191,6 +199,13 @@ std::vector<PriceResult> priceAcrossTime(const Kernel& k, const ModelSpec& model
                                          uint64_t paths, uint64_t seed,
                                          const std::vector<uint64_t>& days, const TEnv& tenv,
                                          unsigned threads = 0);
+// FloatLit values of a kernel in the engine's literal order.
+std::vector<double> kernelFloatLiterals(const Kernel& k);
+std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* literals,
+                                       std::size_t nInstances, std::size_t nLits,
+                                       const ModelSpec& model, uint64_t paths, uint64_t seed,
+                                       const std::vector<uint64_t>& days, const TEnv& tenv,
+                                       const RunOptions& opt = RunOptions());
 // Template batch: instances share one path set (common random numbers, like
 // repeated reference calls with one seed); result [instance * days + d].
 std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,

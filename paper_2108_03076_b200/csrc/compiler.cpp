@@ -303,6 +303,7 @@ class Builder {
 // Specialises one kernel for one valuation day (t_now).
 struct Specializer {
   Builder& B;
+  const std::vector<uint8_t>& litNonZero;  // per variant literal slot
   const Kernel& k;
   const SimPlanHost& plan;
   const std::vector<int32_t>& litNode;  // per kernel node: DAG id of its FloatLit
@@ -503,6 +504,8 @@ struct Specializer {
         if (B.g.isConst(b.v)) {
           if (B.g.rv(b.v) == 0.0) return Val{-1, B.efirst(e, B.cE(dz))};
           ez = -1;
+        } else if (B.g.n[b.v].op == D_LIT && litNonZero[B.g.n[b.v].bits]) {
+          ez = -1;  // a template literal that is non-zero in every instance
         } else {
           ez = B.node(OP_EDIVZ, VT::E, b.v, -1, -1, dz);
         }
@@ -681,33 +684,62 @@ const char* opName(uint32_t op) {
 
 }  // namespace
 
+std::vector<double> kernelLiterals(const Kernel& k) {
+  std::vector<double> v;
+  for (const KNode& n : k.nodes)
+    if (n.kind == KKind::Float) v.push_back(n.real);
+  return v;
+}
+
+LiteralTable literalTableFromInstances(const std::vector<const Kernel*>& instances) {
+  const Kernel& k = *instances.at(0);
+  const uint64_t h0 = kernelShapeHash(k);
+  LiteralTable t;
+  t.nInst = instances.size();
+  for (std::size_t i = 0; i < instances.size(); ++i) {
+    const Kernel& o = *instances[i];
+    if (i > 0 && (o.nodes.size() != k.nodes.size() || kernelShapeHash(o) != h0))
+      throw UnsupportedError("batch instances must share one kernel shape (instance " +
+                             std::to_string(i) + " differs beyond literal values)");
+    std::vector<double> v = kernelLiterals(o);
+    if (i == 0) t.nOcc = v.size();
+    t.values.insert(t.values.end(), v.begin(), v.end());
+  }
+  return t;
+}
+
 CompiledProgram compileProgram(const std::vector<const Kernel*>& instances,
                                const SimPlanHost& plan, const std::vector<uint64_t>& days,
                                const CompileOptions& opt) {
-  const Kernel& k = *instances.at(0);
-  const std::size_t nInst = instances.size();
+  LiteralTable t = literalTableFromInstances(instances);
+  return compileProgram(*instances.at(0), t, plan, days, opt);
+}
+
+CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const SimPlanHost& plan,
+                               const std::vector<uint64_t>& days, const CompileOptions& opt) {
+  const std::size_t nInst = lits.nInst;
+  if (nInst == 0) throw EvalError("no kernel instances");
+  if (lits.nOcc != kernelLiterals(k).size() || lits.values.size() != nInst * lits.nOcc)
+    throw UnsupportedError("literal table does not match the kernel's float literals (" +
+                           std::to_string(lits.nOcc) + " per instance given)");
   // ---- literal slots: FloatLit occurrences deduplicated by their value
   //      vector across instances (shared when equal in every instance).
-  for (std::size_t i = 1; i < nInst; ++i) {
-    const Kernel& o = *instances[i];
-    if (o.nodes.size() != k.nodes.size() || kernelShapeHash(o) != kernelShapeHash(k))
-      throw UnsupportedError("batch instances must share one kernel shape (instance " +
-                             std::to_string(i) + " differs beyond literal values)");
-  }
   Builder B;
   std::vector<int32_t> litNode(k.nodes.size(), -1);
   std::map<std::vector<uint64_t>, uint32_t> slotOf;
   std::vector<std::vector<double>> varSlots;  // variant slot -> values per instance
+  std::size_t occ = 0;
   for (std::size_t idx = 0; idx < k.nodes.size(); ++idx) {
     if (k.nodes[idx].kind != KKind::Float) continue;
     std::vector<uint64_t> vec(nInst);
     bool variant = false;
     for (std::size_t i = 0; i < nInst; ++i) {
-      vec[i] = dbits(instances[i]->nodes[idx].real);
+      vec[i] = dbits(lits.values[i * lits.nOcc + occ]);
       variant = variant || vec[i] != vec[0];
     }
+    ++occ;
     if (!variant) {
-      litNode[idx] = B.cR(k.nodes[idx].real);
+      litNode[idx] = B.cR(bitsd(vec[0]));
       continue;
     }
     auto [it, ins] = slotOf.try_emplace(vec, static_cast<uint32_t>(varSlots.size()));
@@ -718,6 +750,10 @@ CompiledProgram compileProgram(const std::vector<const Kernel*>& instances,
     }
     litNode[idx] = B.lit(it->second);
   }
+  std::vector<uint8_t> litNonZero(varSlots.size(), 1);
+  for (std::size_t v = 0; v < varSlots.size(); ++v)
+    for (double x : varSlots[v])
+      if (x == 0.0) litNonZero[v] = 0;
 
   // ---- specialise each valuation day (priceAcrossTime, pricing.cpp:352-357)
   auto partyIndex = [&](const std::string& p) -> int32_t {
@@ -729,8 +765,8 @@ CompiledProgram compileProgram(const std::vector<const Kernel*>& instances,
   const std::string p2 = k.parties.size() > 1 ? k.parties[1] : "me";
   std::vector<Val> outs;
   for (uint64_t d : days) {
-    Specializer S{B, k, plan, litNode, static_cast<int64_t>(d), partyIndex(p1), partyIndex(p2),
-                  {}, 0};
+    Specializer S{B, litNonZero, k, plan, litNode, static_cast<int64_t>(d), partyIndex(p1),
+                  partyIndex(p2), {}, 0};
     Val r = S.eval(k.root, 0);
     if (r.v >= 0 && B.g.type(r.v) != VT::R)
       r = B.fail(r.e, ErrorCode::Eval, "kernel did not evaluate to a real");
@@ -856,7 +892,12 @@ CompiledProgram compileProgram(const std::vector<const Kernel*>& instances,
     bool inEnd = t >= endBegin;
     for (int32_t ch : {d.a, d.b, d.c}) {
       if (ch < 0 || !needsReg(ch)) continue;
-      lastUse[ch] = std::max(lastUse[ch], inEnd ? T_END : static_cast<int32_t>(t));
+      // a shared value read by the end section (re-run per instance) stays
+      // live to the end; end-section temporaries die at their last read
+      const bool sharedDef = defTime[ch] >= 0 && defTime[ch] < static_cast<int32_t>(endBegin);
+      const bool leaf = defTime[ch] < 0;  // S-slot observable copied by MOV: defTime set
+      lastUse[ch] = std::max(lastUse[ch], (inEnd && (sharedDef || leaf)) ? T_END
+                                                                        : static_cast<int32_t>(t));
     }
   }
   for (int32_t r : rootMap)

@@ -67,6 +67,18 @@ struct CompileOptions {
   bool rewrite = true;
 };
 
+// Template instances: the float literals (FloatLit nodes in node-pool order,
+// i.e. postorder of the kernel JSON tree) of each instance, row-major.
+struct LiteralTable {
+  std::size_t nInst = 0;
+  std::size_t nOcc = 0;
+  std::vector<double> values;  // [nInst][nOcc]
+};
+std::vector<double> kernelLiterals(const Kernel& k);
+LiteralTable literalTableFromInstances(const std::vector<const Kernel*>& instances);
+
+CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const SimPlanHost& plan,
+                               const std::vector<uint64_t>& days, const CompileOptions& opt);
 CompiledProgram compileProgram(const std::vector<const Kernel*>& instances,
                                const SimPlanHost& plan, const std::vector<uint64_t>& days,
                                const CompileOptions& opt);

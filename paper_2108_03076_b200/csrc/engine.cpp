@@ -80,14 +80,36 @@ Plan::Plan(const std::vector<const Kernel*>& instances, const ModelSpec& model,
            const std::vector<uint64_t>& days, const TEnv& tenv, const RunOptions& opt)
     : impl_(new PlanImpl) {
   if (instances.empty()) throw EvalError("no kernel instances");
-  PlanImpl& I = *impl_;
   // Reference order of checks: SimPlan ctor, then the tenv lookups
-  // (proj/src/pricing.cpp:335-338).
+  // (proj/src/pricing.cpp:335-338); then the batch shape check.
   SimPlanHost sp = buildSimPlan(*instances[0], model);
   for (const auto& v : instances[0]->tvars) (void)tenv.lookup(v);
+  LiteralTable t = literalTableFromInstances(instances);
+  init(*instances[0], &t, model, days, tenv, opt);
+}
+
+Plan::Plan(const Kernel& templ, const double* literals, std::size_t nInstances, std::size_t nLits,
+           const ModelSpec& model, const std::vector<uint64_t>& days, const TEnv& tenv,
+           const RunOptions& opt)
+    : impl_(new PlanImpl) {
+  LiteralTable t;
+  t.nInst = nInstances;
+  t.nOcc = nLits;
+  t.values.assign(literals, literals + nInstances * nLits);
+  init(templ, &t, model, days, tenv, opt);
+}
+
+std::vector<double> kernelFloatLiterals(const Kernel& k) { return kernelLiterals(k); }
+
+void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
+                const std::vector<uint64_t>& days, const TEnv& tenv, const RunOptions& opt) {
+  const LiteralTable& lits = *static_cast<const LiteralTable*>(litsv);
+  PlanImpl& I = *impl_;
+  SimPlanHost sp = buildSimPlan(k, model);
+  for (const auto& v : k.tvars) (void)tenv.lookup(v);
   CompileOptions co;
   co.rewrite = opt.rewrite;
-  I.prog = compileProgram(instances, sp, days, co);
+  I.prog = compileProgram(k, lits, sp, days, co);
   I.nOut = I.prog.header.n_instances * I.prog.header.n_days;
 
   int dev = opt.device;
@@ -380,8 +402,19 @@ std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,
                                     const std::vector<uint64_t>& days, const TEnv& tenv,
                                     const RunOptions& opt) {
   if (paths == 0) throw EvalError("path count must be positive");
-  if (days.empty()) return {};
   Plan plan(instances, model, days, tenv, opt);
+  if (days.empty()) return {};
+  return runOnce(plan, paths, seed, days);
+}
+
+std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* literals,
+                                       std::size_t nInstances, std::size_t nLits,
+                                       const ModelSpec& model, uint64_t paths, uint64_t seed,
+                                       const std::vector<uint64_t>& days, const TEnv& tenv,
+                                       const RunOptions& opt) {
+  if (paths == 0) throw EvalError("path count must be positive");
+  Plan plan(templ, literals, nInstances, nLits, model, days, tenv, opt);
+  if (days.empty()) return {};
   return runOnce(plan, paths, seed, days);
 }
 

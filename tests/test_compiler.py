@@ -186,3 +186,19 @@ def test_batch_literal_pool_and_shape_check():
     other = E.Kernel(load_kernel("worst-off"))
     with pytest.raises(E.ContractError, match="share one kernel shape"):
         E.compile_listing([brc, other], m, [0])
+
+
+def test_template_literal_table_matches_instance_batch():
+    brc = E.Kernel(load_kernel("brc"))
+    lits = E.kernel_literals(brc)
+    assert lits == brc.literals() and len(lits) == 1120
+    m = load_model("three")
+    fs = (0.5, 0.65, 0.8)
+    inst = [brc.with_literals({2630.635: 3758.05 * f, 8288.0: 11840.0 * f, 840.0: 1200.0 * f})
+            for f in fs]
+    table = [k.literals() for k in inst]
+    assert all(len(t) == 1120 for t in table)
+    L1 = E.compile_listing(inst, m, [0])
+    assert L1["n_inst_const"] == 3
+    with pytest.raises(E.ContractError, match="literal table does not match"):
+        E.Plan(brc, m, [0], literals=[lits[:-1]])
