@@ -31,11 +31,34 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 # FP64 flops per path of the fused kernel, frozen from the ncu SASS op counters
 # (dadd + dmul + 2*dfma) of the first correct kernel (profiles/).
-F_PATH = {"brc": 286221.4, "worst_off": None, "call": None}
+F_PATH = {"brc": 286221.4, "worst_off": None, "call": None, "brc_batch": None}
 # brc: ncu r1 (profiles/r1_path_kernel_brc_2M_raw.csv), 2e6 paths:
 #   dadd 6.2471e10 + dmul 7.0817e10 + 2 * dfma 2.19577e11 thread-instructions
 
+BATCH_N = 1024
+
+
+def batch_literals(kern_json: str):
+    """C4: 1024 instances of the BRC template -- knock-in barrier at 50%..80%
+    of spot and strike at 90%..110% of spot, in the literal pool only."""
+    import paper_2108_03076_b200 as E
+    base = E.kernel_literals(kern_json)
+    spots = {3758.05: 2630.635, 11840.0: 8288.0, 1200.0: 840.0}  # spot -> 70% barrier
+    rows = []
+    for i in range(BATCH_N):
+        b = 0.5 + 0.3 * i / (BATCH_N - 1)
+        r = 0.9 + 0.2 * ((i * 389) % BATCH_N) / (BATCH_N - 1)
+        sub = {}
+        for sp, bar in spots.items():
+            sub[bar] = sp * b
+            sub[sp] = sp * r
+        rows.append([sub.get(v, v) for v in base])
+    return rows
+
+
 WORKLOADS = {
+    "brc_batch": ("brc", "three", f"C4: {BATCH_N} instances of the BRC template (barrier "
+                  "50-80%, strike 90-110% of spot) on one path set, literals as kernel data"),
     "brc": ("brc", "three", "BRC 3 underlyings x 367 dates (contracts/brc.cl, SURVEY.md App. A)"),
     "worst_off": ("worst-off", "three", "worst-off autocallable 3 x 5 dates (contracts/worst-off.cl)"),
     "call": ("european-call", "call", "European call 1 x 1 date (proj/contracts/european-call.cl)"),
@@ -187,7 +210,9 @@ def main():
     kern = E.Kernel(kern_json)
     paths = args.paths_per_gpu * world
     seed = 42
-    pricer = DistributedPricer(kern, model_json, [0], device=local)
+    literals = batch_literals(kern_json) if args.workload == "brc_batch" else None
+    n_inst = len(literals) if literals else 1
+    pricer = DistributedPricer(kern, model_json, [0], device=local, literals=literals)
     info = pricer.plan.info
     dev = torch.device(f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -237,7 +262,7 @@ def main():
         tt = torch.tensor([t_step, t_kern], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_kern = float(tt[0]), float(tt[1])
-    value = paths / (t_step * 1e-3)
+    value = paths * n_inst / (t_step * 1e-3)  # instance-paths/s (= paths/s for one contract)
 
     # end to end through the public API, host JSON in -> host results out
     e2e_times = []
@@ -246,7 +271,9 @@ def main():
         t0 = time.perf_counter()
         if world > 1:
             from paper_2108_03076_b200 import distributed as D
-            D.price(E.Kernel(kern_json), model_json, paths, seed)
+            D.price(E.Kernel(kern_json), model_json, paths, seed, literals=literals)
+        elif literals is not None:
+            E.price_template(kern_json, literals, model_json, paths, seed)
         else:
             E.price(kern_json, model_json, paths, seed)
         torch.cuda.synchronize(dev)
@@ -265,7 +292,7 @@ def main():
     fpath = F_PATH.get(args.workload)
     per_gpu_paths = paths / world
     if fpath:
-        achieved = per_gpu_paths * fpath / (t_kern * 1e-3) / 1e12
+        achieved = per_gpu_paths * n_inst * fpath / (t_kern * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / peak_tflops, "traffic": None,
                 "peak_source": "measured DFMA microbenchmark (cltk_fp64_peak), this GPU, burst",
@@ -277,7 +304,7 @@ def main():
                 "f_path": None, "note": "F_path not yet frozen from ncu"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and literals is None:
         threads = os.cpu_count() or 1
         kind, dt, r = cpu_reference(kern_json, model_json, args.ref_paths, seed, threads)
         cpu = {"value": args.ref_paths / dt, "unit": "paths/s", "cores": threads, "kind": kind,
@@ -290,14 +317,14 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": desc, "paths_per_gpu": args.paths_per_gpu,
+                "config": {"workload": desc, "instances": n_inst, "paths_per_gpu": args.paths_per_gpu,
                            "paths_per_step": paths, "seed": seed, "rng": "philox2x64-10",
                            "parallelism": f"paths sharded over {world} GPU(s), 1 all_reduce",
                            "l2": "flushed between timed steps (256 MiB write); inputs are a "
                                  f"{h2d} B compiled program",
                            "kernel_ms": t_kern},
                 "roofline": roof, "cpu_baseline": cpu,
-                "e2e": {"value": paths / t_e2e if t_e2e > 0 else None, "unit": "paths/s",
+                "e2e": {"value": paths * n_inst / t_e2e if t_e2e > 0 else None, "unit": "paths/s",
                         "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h,
                         "path": "paper_2108_03076_b200.price -> cltk_gpu_price (C-ABI), host "
