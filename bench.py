@@ -31,9 +31,10 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 # FP64 flops per path of the fused kernel, frozen from the ncu SASS op counters
 # (dadd + dmul + 2*dfma) of the first correct kernel (profiles/).
-F_PATH = {"brc": 286221.4, "worst_off": None, "call": None, "brc_batch": None}
+F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None}
 # brc: ncu r1 (profiles/r1_path_kernel_brc_2M_raw.csv), 2e6 paths:
 #   dadd 6.2471e10 + dmul 7.0817e10 + 2 * dfma 2.19577e11 thread-instructions
+# worst_off / call: first measurement (profiles/r1_fp64ops_*_2M.csv), 2e6 paths
 
 BATCH_N = 1024
 

@@ -164,6 +164,9 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 #ifndef CLTK_MAX_BATCH
 #define CLTK_MAX_BATCH 6
 #endif
+#ifndef CLTK_ILP2
+#define CLTK_ILP2 1
+#endif
 #ifndef CLTK_MIN_BLOCKS
 #define CLTK_MIN_BLOCKS 5
 #endif
@@ -290,14 +293,14 @@ __device__ __forceinline__ bool normals_batch(const PhiloxKeys& K, uint64_t path
     return b;
   };
   int m = 0;
-  for (; m + 1 < M; m += 2) {
+  for (; CLTK_ILP2 && m + 1 < M; m += 2) {
     const uint64_t b0 = phase1(m), b1 = phase1(m + 1);
     if ((drawMask >> m) & 1u) ok = ok && ((b0 >> 11) != 0x1FFFFFFFFFFFFFULL);
     if ((drawMask >> (m + 1)) & 1u) ok = ok && ((b1 >> 11) != 0x1FFFFFFFFFFFFFULL);
     list_push(tails, nTail, !acklam_is_central(NS.P[m * kBlock + tid]), m, lane);
     list_push(tails, nTail, !acklam_is_central(NS.P[(m + 1) * kBlock + tid]), m + 1, lane);
   }
-  if (m < M) {
+  for (; m < M; ++m) {
     const uint64_t b0 = phase1(m);
     if ((drawMask >> m) & 1u) ok = ok && ((b0 >> 11) != 0x1FFFFFFFFFFFFFULL);
     list_push(tails, nTail, !acklam_is_central(NS.P[m * kBlock + tid]), m, lane);
@@ -314,14 +317,14 @@ __device__ __forceinline__ bool normals_batch(const PhiloxKeys& K, uint64_t path
     NS.Y[q * kBlock + tid] = r == cltk_gm::ERFC_R1 ? v : y;
     return r;
   };
-  for (m = 0; m + 1 < M; m += 2) {
+  for (m = 0; CLTK_ILP2 && m + 1 < M; m += 2) {
     const int ra = phase3(m), rb = phase3(m + 1);
     list_push(r2, n2, ra == cltk_gm::ERFC_R2, m, lane);
     list_push(r3, n3, ra == cltk_gm::ERFC_REST, m, lane);
     list_push(r2, n2, rb == cltk_gm::ERFC_R2, m + 1, lane);
     list_push(r3, n3, rb == cltk_gm::ERFC_REST, m + 1, lane);
   }
-  if (m < M) {
+  for (; m < M; ++m) {
     const int ra = phase3(m);
     list_push(r2, n2, ra == cltk_gm::ERFC_R2, m, lane);
     list_push(r3, n3, ra == cltk_gm::ERFC_REST, m, lane);
@@ -340,11 +343,11 @@ __device__ __forceinline__ bool normals_batch(const PhiloxKeys& K, uint64_t path
     const int o = q * kBlock + tid;
     NS.X[o] = halley(NS.X[o], NS.P[o], NS.Y[o]);
   };
-  for (m = 0; m + 1 < M; m += 2) {
+  for (m = 0; CLTK_ILP2 && m + 1 < M; m += 2) {
     phase5(m);
     phase5(m + 1);
   }
-  if (m < M) phase5(m);
+  for (; m < M; ++m) phase5(m);
   return ok;
 }
 
