@@ -165,10 +165,10 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 #define CLTK_MAX_BATCH 6
 #endif
 #ifndef CLTK_ILP2
-#define CLTK_ILP2 1
+#define CLTK_ILP2 0
 #endif
 #ifndef CLTK_MIN_BLOCKS
-#define CLTK_MIN_BLOCKS 5
+#define CLTK_MIN_BLOCKS 6
 #endif
 constexpr int kMaxBatch = CLTK_MAX_BATCH;
 // doubles: X, P, Y slots + the per-warp work lists (3 * 32 * kMaxBatch u16)
