@@ -15,7 +15,7 @@ CXXFLAGS := -std=c++17 -O2 -fPIC -ffp-contract=off -Wall -Wno-unused-function \
 NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -ccbin $(HOSTCXX) \
             -Xcompiler -fPIC -Xptxas -v -Iinclude
 
-HOST_SRCS := host_model compiler engine capi
+HOST_SRCS := host_model compiler engine capi sobol_table
 HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS)))
 CU_OBJS   := $(OBJ)/mc_engine.o
 HDRS      := $(wildcard $(SRC)/*.hpp $(SRC)/*.h) include/cltk_b200.h

@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--ref-paths", type=int, default=100_000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rng", default="philox", choices=["philox", "sobol"],
+                    help="philox: the reference's generator (bit-exact parity); sobol: QMC mode")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -213,7 +215,7 @@ def main():
     seed = 42
     literals = batch_literals(kern_json) if args.workload == "brc_batch" else None
     n_inst = len(literals) if literals else 1
-    pricer = DistributedPricer(kern, model_json, [0], device=local, literals=literals)
+    pricer = DistributedPricer(kern, model_json, [0], device=local, literals=literals, rng=args.rng)
     info = pricer.plan.info
     dev = torch.device(f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -272,11 +274,11 @@ def main():
         t0 = time.perf_counter()
         if world > 1:
             from paper_2108_03076_b200 import distributed as D
-            D.price(E.Kernel(kern_json), model_json, paths, seed, literals=literals)
+            D.price(E.Kernel(kern_json), model_json, paths, seed, literals=literals, rng=args.rng)
         elif literals is not None:
-            E.price_template(kern_json, literals, model_json, paths, seed)
+            E.price_template(kern_json, literals, model_json, paths, seed, rng=args.rng)
         else:
-            E.price(kern_json, model_json, paths, seed)
+            E.price(kern_json, model_json, paths, seed, rng=args.rng)
         torch.cuda.synchronize(dev)
         e2e_times.append(time.perf_counter() - t0)
     t_e2e = sum(e2e_times) / max(1, len(e2e_times))
@@ -290,7 +292,7 @@ def main():
     d2h = info["n_outputs"] * 24 + 8
 
     # roofline: FP64 pipe (the kernel reads only constants; no HBM term)
-    fpath = F_PATH.get(args.workload)
+    fpath = F_PATH.get(args.workload) if args.rng == "philox" else None
     per_gpu_paths = paths / world
     if fpath:
         achieved = per_gpu_paths * n_inst * fpath / (t_kern * 1e-3) / 1e12
@@ -319,7 +321,9 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": desc, "instances": n_inst, "paths_per_gpu": args.paths_per_gpu,
-                           "paths_per_step": paths, "seed": seed, "rng": "philox2x64-10",
+                           "paths_per_step": paths, "seed": seed,
+                           "rng": "philox2x64-10 (reference generator, bit-exact)" if args.rng == "philox"
+                           else "sobol (Joe-Kuo) + AS241 + Brownian bridge (QMC)",
                            "parallelism": f"paths sharded over {world} GPU(s), 1 all_reduce",
                            "l2": "flushed between timed steps (256 MiB write); inputs are a "
                                  f"{h2d} B compiled program",

@@ -64,6 +64,17 @@ typedef struct {
   double n, mean, m2;
 } cltk_partial_t;
 
+/* Engine options.  rng: 0 = Philox2x64-10 + Acklam/Halley (the reference's
+ * generator; bit-exact per path), 1 = Sobol (Joe-Kuo, 32-bit) + Wichura AS241
+ * + Brownian bridge over the drawing days (QMC; seed != 0 applies a
+ * per-dimension digital shift).  rewrite: exact OR/AND->min/max rewrite. */
+typedef struct {
+  int device;   /* -1: current */
+  int rewrite;  /* default 1 */
+  int rng;      /* default 0 */
+  int reserved[5];
+} cltk_options;
+
 const char* cltk_version(void);
 
 /* priceAcrossTime: results[n_days].  `threads` is accepted and ignored (the
@@ -95,7 +106,19 @@ int cltk_gpu_price_template(const char* kernel_json, const double* literals, siz
 int cltk_kernel_literals(const char* kernel_json, double* out, size_t cap, size_t* n,
                          cltk_error* err);
 
+/* Everything above with options: literals == NULL prices the kernel alone
+ * (n_instances must be 1), else literals[n_instances][n_literals] as in
+ * cltk_gpu_price_template.  opts == NULL: defaults. */
+int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_instances,
+                      size_t n_literals, const char* model_json, uint64_t paths, uint64_t seed,
+                      const uint64_t* days, size_t n_days, const char* tenv_json,
+                      const cltk_options* opts, cltk_price_result* results, cltk_error* err);
+
 /* ---- plan API: compile once, launch chunk ranges, combine --------------- */
+int cltk_plan_create_ex(const char* kernel_json, const double* literals, size_t n_instances,
+                        size_t n_literals, const char* model_json, const uint64_t* days,
+                        size_t n_days, const char* tenv_json, const cltk_options* opts,
+                        cltk_plan** plan, cltk_error* err);
 int cltk_plan_create_template(const char* kernel_json, const double* literals, size_t n_instances,
                               size_t n_literals, const char* model_json, const uint64_t* days,
                               size_t n_days, const char* tenv_json, int device, int rewrite,
@@ -128,7 +151,8 @@ int cltk_plan_set_error_word(cltk_plan* plan, void* stream, uint64_t word);
  * the engine's analogue of emitKernelSource (proj/src/kernel.cpp:407). */
 int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
                          const char* model_json, const uint64_t* days, size_t n_days,
-                         const char* tenv_json, int rewrite, char** json, cltk_error* err);
+                         const char* tenv_json, int rewrite, int rng, char** json,
+                         cltk_error* err);
 /* Program listing (JSON, malloc'd; free with cltk_free). */
 int cltk_plan_dump(const cltk_plan* plan, char** json);
 void cltk_free(void* p);

@@ -184,24 +184,43 @@ def _results(arr, n: int) -> list[dict]:
                  seed=arr[i].seed, valuation_day=arr[i].valuation_day) for i in range(n)]
 
 
+RNG_MODES = {"philox": 0, "sobol": 1}
+
+
+def _options(device: int = -1, rewrite: bool = True, rng: str = "philox"):
+    if rng not in RNG_MODES:
+        raise ValueError(f"rng must be one of {sorted(RNG_MODES)}")
+    o = _native.OptionsC()
+    o.device, o.rewrite, o.rng = int(device), int(bool(rewrite)), RNG_MODES[rng]
+    return o
+
+
 def version() -> str:
     return _native.lib().cltk_version().decode()
 
 
 def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, seed: int = 0,
           days: Sequence[int] = (0,), tenv: dict | None = None, threads: int = 0,
-          device: int = -1) -> list[dict]:
+          device: int = -1, rng: str = "philox") -> list[dict]:
     """priceAcrossTime on the GPU (cltk.price, proj/python/bindings.cpp:103-126).
 
     Returns one dict per valuation day: ``price``, ``std_error``, ``paths``,
     ``seed``, ``valuation_day``.  ``threads`` is accepted for compatibility
-    (results never depend on it)."""
+    (results never depend on it).  ``rng="philox"`` (default) reproduces the
+    reference's per-path values bit for bit; ``rng="sobol"`` is the QMC mode
+    (Sobol + AS241 + Brownian bridge)."""
     L = _native.lib()
     d, nd = _days(days)
     out = (_native.PriceResultC * max(1, nd))()
     err = _native.ErrorC()
-    rc = L.cltk_gpu_price(_kernel_json(kernel), _model_json(model), int(paths), int(seed), d, nd,
-                          _tenv_json(tenv), int(threads), int(device), out, C.byref(err))
+    if rng == "philox":
+        rc = L.cltk_gpu_price(_kernel_json(kernel), _model_json(model), int(paths), int(seed), d,
+                              nd, _tenv_json(tenv), int(threads), int(device), out, C.byref(err))
+    else:
+        o = _options(device, True, rng)
+        rc = L.cltk_gpu_price_ex(_kernel_json(kernel), None, 1, 0, _model_json(model), int(paths),
+                                 int(seed), d, nd, _tenv_json(tenv), C.byref(o), out,
+                                 C.byref(err))
     _raise(rc, err)
     return _results(out, nd)
 
@@ -239,7 +258,8 @@ def kernel_literals(kernel: Kernel | str | dict) -> list[float]:
 
 def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
                    paths: int = 100000, seed: int = 0, days: Sequence[int] = (0,),
-                   tenv: dict | None = None, device: int = -1) -> list[list[dict]]:
+                   tenv: dict | None = None, device: int = -1,
+                   rng: str = "philox") -> list[list[dict]]:
     """Price instances of one template given as a literal table
     ``literals[instance][j]`` (j in ``kernel_literals`` order): one compile,
     one path set, the literals passed to the kernel as data."""
@@ -252,9 +272,10 @@ def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
     n = lit.shape[0]
     out = (_native.PriceResultC * max(1, n * nd))()
     err = _native.ErrorC()
-    rc = L.cltk_gpu_price_template(_kernel_json(kernel), lit.ctypes.data, n, lit.shape[1],
-                                   _model_json(model), int(paths), int(seed), d, nd,
-                                   _tenv_json(tenv), int(device), out, C.byref(err))
+    o = _options(device, True, rng)
+    rc = L.cltk_gpu_price_ex(_kernel_json(kernel), lit.ctypes.data, n, lit.shape[1],
+                             _model_json(model), int(paths), int(seed), d, nd, _tenv_json(tenv),
+                             C.byref(o), out, C.byref(err))
     _raise(rc, err)
     flat = _results(out, n * nd)
     return [flat[i * nd:(i + 1) * nd] for i in range(n)]
@@ -267,7 +288,7 @@ def black_scholes_call(spot: float, strike: float, rate: float, vol: float,
 
 def compile_listing(kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
                     days: Sequence[int] = (0,), tenv: dict | None = None,
-                    rewrite: bool = True) -> dict:
+                    rewrite: bool = True, rng: str = "philox") -> dict:
     """Host-only compile: the streaming device program as JSON (no GPU needed)."""
     if not isinstance(kernels, (list, tuple)):
         kernels = [kernels]
@@ -277,7 +298,7 @@ def compile_listing(kernels: Sequence[Kernel | str | dict] | Kernel, model: str 
     out = C.c_void_p()
     err = _native.ErrorC()
     rc = L.cltk_compile_listing(arr, len(kernels), _model_json(model), d, nd, _tenv_json(tenv),
-                                int(rewrite), C.byref(out), C.byref(err))
+                                int(rewrite), RNG_MODES[rng], C.byref(out), C.byref(err))
     _raise(rc, err)
     s = C.cast(out, C.c_char_p).value.decode()
     L.cltk_free(out)
@@ -290,7 +311,7 @@ class Plan:
 
     def __init__(self, kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
                  days: Sequence[int] = (0,), tenv: dict | None = None, device: int = -1,
-                 rewrite: bool = True, literals=None):
+                 rewrite: bool = True, literals=None, rng: str = "philox"):
         if not isinstance(kernels, (list, tuple)):
             kernels = [kernels]
         self._L = _native.lib()
@@ -298,13 +319,19 @@ class Plan:
         d, nd = _days(self.days)
         self._h = C.c_void_p()
         err = _native.ErrorC()
-        if literals is not None:
+        if literals is not None or rng != "philox":
             import numpy as np
-            lit = np.ascontiguousarray(literals, dtype=np.float64)
-            rc = self._L.cltk_plan_create_template(
-                _kernel_json(kernels[0]), lit.ctypes.data, lit.shape[0], lit.shape[1],
-                _model_json(model), d, nd, _tenv_json(tenv), int(device), int(rewrite),
-                C.byref(self._h), C.byref(err))
+            o = _options(device, rewrite, rng)
+            if literals is not None:
+                lit = np.ascontiguousarray(literals, dtype=np.float64)
+                lp, n_i, n_l = lit.ctypes.data, lit.shape[0], lit.shape[1]
+            else:
+                lit, lp, n_i, n_l = None, None, 1, 0
+            if len(kernels) != 1:
+                raise ValueError("rng/literals plans take one template kernel")
+            rc = self._L.cltk_plan_create_ex(
+                _kernel_json(kernels[0]), lp, n_i, n_l, _model_json(model), d, nd,
+                _tenv_json(tenv), C.byref(o), C.byref(self._h), C.byref(err))
         else:
             arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
             rc = self._L.cltk_plan_create(arr, len(kernels), _model_json(model), d, nd,

@@ -19,8 +19,14 @@ EXPORTS = [
     "cltk_plan_finalize", "cltk_plan_error_word", "cltk_plan_set_error_word",
     "cltk_compile_listing", "cltk_plan_dump", "cltk_free", "cltk_debug_paths", "cltk_debug_rng", "cltk_debug_math",
     "cltk_fp64_peak", "cltk_black_scholes_call", "cltk_gpu_price_template",
-    "cltk_kernel_literals", "cltk_plan_create_template",
+    "cltk_kernel_literals", "cltk_plan_create_template", "cltk_gpu_price_ex",
+    "cltk_plan_create_ex",
 ]
+
+
+class OptionsC(C.Structure):
+    _fields_ = [("device", C.c_int), ("rewrite", C.c_int), ("rng", C.c_int),
+                ("reserved", C.c_int * 5)]
 
 
 class PriceResultC(C.Structure):
@@ -88,7 +94,14 @@ def lib() -> C.CDLL:
     L.cltk_plan_set_error_word.argtypes = [vp, vp, u64]
     L.cltk_compile_listing.restype = i32
     L.cltk_compile_listing.argtypes = [C.POINTER(cp), C.c_size_t, cp, P64, C.c_size_t, cp, i32,
-                                       C.POINTER(vp), PE]
+                                       i32, C.POINTER(vp), PE]
+    PO = C.POINTER(OptionsC)
+    L.cltk_gpu_price_ex.restype = i32
+    L.cltk_gpu_price_ex.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, u64, u64, P64, C.c_size_t,
+                                    cp, PO, PR, PE]
+    L.cltk_plan_create_ex.restype = i32
+    L.cltk_plan_create_ex.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t, cp, PO,
+                                      C.POINTER(vp), PE]
     L.cltk_plan_dump.restype = i32
     L.cltk_plan_dump.argtypes = [vp, C.POINTER(vp)]
     L.cltk_free.argtypes = [vp]

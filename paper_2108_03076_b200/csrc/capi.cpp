@@ -148,6 +148,63 @@ int cltk_plan_create_template(const char* kernel_json, const double* literals, s
   });
 }
 
+namespace {
+RunOptions optionsOf(const cltk_options* o) {
+  RunOptions r;
+  if (o) {
+    r.device = o->device;
+    r.rewrite = o->rewrite != 0;
+    r.rng = o->rng;
+  }
+  return r;
+}
+}  // namespace
+
+int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_instances,
+                      size_t n_literals, const char* model_json, uint64_t paths, uint64_t seed,
+                      const uint64_t* days, size_t n_days, const char* tenv_json,
+                      const cltk_options* opts, cltk_price_result* results, cltk_error* err) {
+  return guarded(err, [&] {
+    if (paths == 0) throw EvalError("path count must be positive");
+    Kernel k = kernelFromJson(kernel_json);
+    ModelSpec m = modelFromJson(model_json);
+    std::vector<uint64_t> d(days, days + n_days);
+    RunOptions opt = optionsOf(opts);
+    std::vector<double> own;
+    if (!literals) {
+      own = kernelFloatLiterals(k);
+      literals = own.data();
+      n_instances = 1;
+      n_literals = own.size();
+    }
+    toC(priceTemplate(k, literals, n_instances, n_literals, m, paths, seed, d, tenvOf(tenv_json),
+                      opt),
+        results);
+  });
+}
+
+int cltk_plan_create_ex(const char* kernel_json, const double* literals, size_t n_instances,
+                        size_t n_literals, const char* model_json, const uint64_t* days,
+                        size_t n_days, const char* tenv_json, const cltk_options* opts,
+                        cltk_plan** out, cltk_error* err) {
+  return guarded(err, [&] {
+    auto p = std::make_unique<cltk_plan>();
+    p->kernels.push_back(std::make_unique<Kernel>(kernelFromJson(kernel_json)));
+    std::vector<double> own;
+    if (!literals) {
+      own = kernelFloatLiterals(*p->kernels[0]);
+      literals = own.data();
+      n_instances = 1;
+      n_literals = own.size();
+    }
+    ModelSpec m = modelFromJson(model_json);
+    p->plan = std::make_unique<Plan>(*p->kernels[0], literals, n_instances, n_literals, m,
+                                     std::vector<uint64_t>(days, days + n_days),
+                                     tenvOf(tenv_json), optionsOf(opts));
+    *out = p.release();
+  });
+}
+
 int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const char* model_json,
                      const uint64_t* days, size_t n_days, const char* tenv_json, int device,
                      int rewrite, cltk_plan** out, cltk_error* err) {
@@ -234,7 +291,8 @@ int cltk_fp64_peak(int device, int iters, double* tflops, double* seconds, cltk_
 
 int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
                          const char* model_json, const uint64_t* days, size_t n_days,
-                         const char* tenv_json, int rewrite, char** json, cltk_error* err) {
+                         const char* tenv_json, int rewrite, int rng, char** json,
+                         cltk_error* err) {
   return guarded(err, [&] {
     std::vector<Kernel> ks;
     ks.reserve(n_instances);
@@ -243,7 +301,7 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
     for (auto& k : ks) ptrs.push_back(&k);
     if (ptrs.empty()) throw EvalError("no kernel instances");
     ModelSpec m = modelFromJson(model_json);
-    SimPlanHost sp = buildSimPlan(*ptrs[0], m);
+    SimPlanHost sp = buildSimPlan(*ptrs[0], m, static_cast<uint32_t>(rng));
     TEnv t = tenvOf(tenv_json);
     for (const auto& v : ptrs[0]->tvars) (void)t.lookup(v);
     CompileOptions co;

@@ -132,6 +132,10 @@ std::string priceResultToJson(const PriceResult& r);
 struct RunOptions {
   int device = -1;      // -1: current device
   bool rewrite = true;  // OR/AND-of-compare -> running min/max (exact)
+  // 0: Philox2x64-10 + Acklam/Halley (the reference's generator, bit-exact);
+  // 1: Sobol (Joe-Kuo, 32-bit) + Wichura AS241 + Brownian bridge (QMC;
+  //    seed != 0 applies a Philox-derived digital shift per dimension).
+  int rng = 0;
 };
 
 // ---- compiled plan (host + device state) ------------------------------------

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <cstring>
 #include <nlohmann/json.hpp>
 #include <sstream>
@@ -16,8 +17,119 @@ namespace b200 {
 // ---------------------------------------------------------------------------
 // SimPlan (proj/src/pricing.cpp:173-212, 214-253)
 // ---------------------------------------------------------------------------
-SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& model) {
+namespace {
+
+// QMC mode: Brownian bridge over the drawing steps' times tau (years from
+// day 0).  Nodes are numbered breadth-first (node 0 = W(T), then interval
+// midpoints level by level -- the order that gives the low Sobol
+// dimensions to the coarse structure); the device evaluates them in a
+// pre-order traversal that *emits* W(tau_s) in time order, so the path is
+// streamed with O(log n) live values (slots) instead of being materialised.
+void buildBridge(SimPlanHost& p, const std::vector<uint32_t>& drawSteps,
+                 const std::vector<double>& tau) {
+  const int nD = static_cast<int>(drawSteps.size());
+  if (nD == 0) return;
+  std::vector<int> node(nD, -1), L(nD, -2), R(nD, -2);
+  auto T = [&](int i) { return i < 0 ? 0.0 : tau[i]; };
+  node[nD - 1] = 0;
+  int next = 1;
+  std::vector<std::pair<int, int>> q{{-1, nD - 1}};
+  for (std::size_t h = 0; h < q.size(); ++h) {
+    auto [l, r] = q[h];
+    if (r - l < 2) continue;
+    const int m = l + (r - l) / 2;
+    node[m] = next++;
+    L[m] = l;
+    R[m] = r;
+    q.push_back({l, m});
+    q.push_back({m, r});
+  }
+  // traversal: COMPUTE in pre-order, EMIT in order (= time order)
+  struct Ev {
+    bool emit;
+    int m;
+  };
+  std::vector<Ev> seq{{false, nD - 1}};
+  // iterative in-order over the bisection tree of (-1, nD-1)
+  std::function<void(int, int)> visit = [&](int l, int r) {
+    if (r - l < 2) return;
+    const int m = l + (r - l) / 2;
+    seq.push_back({false, m});
+    visit(l, m);
+    seq.push_back({true, m});
+    visit(m, r);
+  };
+  visit(-1, nD - 1);
+  seq.push_back({true, nD - 1});
+  // last use of every point: its emit, or a compute that reads it
+  std::vector<int> lastUse(nD, -1);
+  for (int t = 0; t < static_cast<int>(seq.size()); ++t) {
+    const Ev& e = seq[t];
+    if (e.emit) {
+      lastUse[e.m] = std::max(lastUse[e.m], t);
+    } else {
+      if (L[e.m] >= 0) lastUse[L[e.m]] = std::max(lastUse[L[e.m]], t);
+      if (R[e.m] >= 0) lastUse[R[e.m]] = std::max(lastUse[R[e.m]], t);
+    }
+  }
+  std::vector<int> slot(nD, -1), freeSlots;
+  int nSlots = 0;
+  uint32_t emitted = 0;
+  std::vector<std::vector<int>> releaseAt(seq.size() + 1);
+  for (int t = 0; t < static_cast<int>(seq.size()); ++t) {
+    const Ev& e = seq[t];
+    if (!e.emit) {
+      int s;
+      if (!freeSlots.empty()) {
+        s = freeSlots.back();
+        freeSlots.pop_back();
+      } else {
+        s = nSlots++;
+      }
+      slot[e.m] = s;
+      cltk_bridge_op op{};
+      const int l = L[e.m], r = R[e.m];
+      if (e.m == nD - 1) {  // W(T) = sqrt(T) Z
+        op.wl = 0.0;
+        op.wr = 0.0;
+        op.sd = std::sqrt(T(nD - 1));
+        op.l = op.r = CLTK_BR_ORIGIN;
+      } else {
+        const double tl = T(l), tr = T(r), tm = T(e.m);
+        op.wl = (tr - tm) / (tr - tl);
+        op.wr = (tm - tl) / (tr - tl);
+        op.sd = std::sqrt((tm - tl) * (tr - tm) / (tr - tl));
+        op.l = l < 0 ? CLTK_BR_ORIGIN : static_cast<uint16_t>(slot[l]);
+        op.r = static_cast<uint16_t>(slot[r]);
+      }
+      op.dst = static_cast<uint16_t>(s);
+      op.node = static_cast<uint32_t>(node[e.m]);
+      p.bridge.push_back(op);
+    } else {
+      cltk_step& st = p.steps[drawSteps[emitted]];
+      st.br_end = static_cast<uint32_t>(p.bridge.size());
+      st.br_emit = static_cast<uint32_t>(slot[e.m]);
+      if (emitted + 1 < drawSteps.size())
+        p.steps[drawSteps[emitted + 1]].br_begin = static_cast<uint32_t>(p.bridge.size());
+      ++emitted;
+    }
+    // free the slots whose last use was this event (after it executed)
+    if (e.emit) {
+      if (lastUse[e.m] == t) freeSlots.push_back(slot[e.m]);
+    } else {
+      for (int x : {L[e.m], R[e.m]})
+        if (x >= 0 && lastUse[x] == t) freeSlots.push_back(slot[x]);
+    }
+  }
+  p.steps[drawSteps[0]].br_begin = 0;
+  p.bridgeSlots = static_cast<uint32_t>(nSlots);
+}
+
+}  // namespace
+
+SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& model, uint32_t rng) {
   SimPlanHost p;
+  p.rng = rng;
   p.days = k.rows;
   std::sort(p.days.begin(), p.days.end());
   p.days.erase(std::unique(p.days.begin(), p.days.end()), p.days.end());
@@ -79,6 +191,28 @@ SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& model) {
     p.steps.push_back(st);
   }
   for (uint32_t a : p.colToAsset) p.usedMask |= 1u << a;
+  if (rng == CLTK_RNG_SOBOL) {
+    // Same GBM in closed form over the bridge's W(t): logS(t) = log(spot)
+    // + (drift - vol^2/2) t + vol (L W(t))
+    std::vector<uint32_t> drawSteps;
+    std::vector<double> tau;
+    for (std::size_t s = 0; s < p.steps.size(); ++s) {
+      if (p.steps[s].draws != STEP_DRAW) continue;
+      const double t = static_cast<double>(p.days[s]) / model.dayCount;
+      drawSteps.push_back(static_cast<uint32_t>(s));
+      tau.push_back(t);
+      for (std::size_t j = 0; j < n; ++j) {
+        const AssetSpec& a = *spec[j];
+        p.steps[s].A[j] = (a.drift - 0.5 * a.vol * a.vol) * t;
+        p.steps[s].B[j] = a.vol;
+      }
+    }
+    if (drawSteps.size() * n > CLTK_SOBOL_MAX_DIMS)
+      throw UnsupportedError("Sobol mode supports at most " + std::to_string(CLTK_SOBOL_MAX_DIMS) +
+                             " dimensions (drawing days x assets); this plan needs " +
+                             std::to_string(drawSteps.size() * n));
+    buildBridge(p, drawSteps, tau);
+  }
   return p;
 }
 
@@ -971,6 +1105,7 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   // ---- emit
   CompiledProgram P;
   P.steps = plan.steps;
+  P.bridge = plan.bridge;
   for (std::size_t t = 0; t < linear.size(); ++t) {
     const Ins& x = linear[t];
     const DNode& d = g.n[x.node];
@@ -1019,6 +1154,9 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   h.inst_code_end = static_cast<uint32_t>(linear.size());
   h.has_err = hasErr;
   h.used_mask = plan.usedMask;
+  h.rng = plan.rng;
+  h.n_bridge_slots = plan.bridgeSlots;
+  h.n_bridge_ops = static_cast<uint32_t>(plan.bridge.size());
   std::memcpy(h.chol, plan.chol, sizeof h.chol);
   std::memcpy(h.logS0, plan.logS0, sizeof h.logS0);
   P.kernelNodes = k.nodes.size();
@@ -1044,10 +1182,17 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
       Sv.push_back(s.S[j]);
     }
     st.push_back({{"kind", s.draws}, {"begin", s.code_begin}, {"end", s.code_end},
-                  {"A", A}, {"B", Bv}, {"S", Sv}});
+                  {"A", A}, {"B", Bv}, {"S", Sv}, {"br", {s.br_begin, s.br_end, s.br_emit}}});
   }
   L["steps"] = st;
   L["days"] = plan.days;
+  L["rng"] = plan.rng;
+  L["bridge_slots"] = plan.bridgeSlots;
+  Json br = Json::array();
+  for (const auto& b : plan.bridge)
+    br.push_back({b.node, b.dst, b.l == CLTK_BR_ORIGIN ? -1 : (int)b.l,
+                  b.r == CLTK_BR_ORIGIN ? -1 : (int)b.r, b.wl, b.wr, b.sd});
+  L["bridge"] = br;
   Json sc = Json::array();
   for (double v : P.sharedConst) sc.push_back(dbits(v));
   L["shared_const_bits"] = sc;

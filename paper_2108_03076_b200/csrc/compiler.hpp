@@ -39,8 +39,11 @@ struct SimPlanHost {
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS] = {0};
   double logS0[CLTK_MAX_ASSETS] = {0};
   uint32_t usedMask = 0;
+  uint32_t rng = CLTK_RNG_PHILOX;
+  std::vector<cltk_bridge_op> bridge;  // QMC mode: construction ops in traversal order
+  uint32_t bridgeSlots = 0;
 };
-SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& m);
+SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& m, uint32_t rng = CLTK_RNG_PHILOX);
 
 struct ErrorSite {
   ErrorCode code;
@@ -51,6 +54,7 @@ struct ErrorSite {
 enum : uint32_t { STEP_CONST_S = 0, STEP_DRAW = 1, STEP_EXP_ONLY = 2 };
 
 struct CompiledProgram {
+  std::vector<cltk_bridge_op> bridge;  // QMC mode
   std::vector<uint64_t> code;          // shared ops (step-ordered) then instance ops
   std::vector<cltk_step> steps;        // simulation constants + shared-op ranges
   std::vector<double> sharedConst;     // bit patterns for B/I/E constants

@@ -34,12 +34,28 @@ T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
 }
 
 constexpr uint64_t kMaxChunks = 1ULL << 20;
+
+// Philox2x64-10 on the host (QMC digital shifts only).
+uint64_t philoxHost(uint64_t key, uint64_t c0, uint64_t c1) {
+  for (int r = 0; r < 10; ++r) {
+    const unsigned __int128 prod = static_cast<unsigned __int128>(0xD2B74407B1CE6E93ULL) * c0;
+    c0 = static_cast<uint64_t>(prod >> 64) ^ key ^ c1;
+    c1 = static_cast<uint64_t>(prod);
+    key += 0x9E3779B97F4A7C15ULL;
+  }
+  return c0 ^ c1;
+}
 constexpr uint64_t kPartialBudget = 1ULL << 30;  // bytes of chunk partials
 
 }  // namespace
 
+extern const uint32_t kSobolDims;  // sobol_table.cpp (generated)
+extern const uint32_t kSobolV[];
+
 struct PlanImpl {
   CompiledProgram prog;
+  uint32_t* sobolShift = nullptr;  // device [kSobolDims], for shiftSeed
+  uint64_t shiftSeed = 0;
   DevPlan dev{};
   int device = 0;
   int sms = 0;
@@ -82,7 +98,7 @@ Plan::Plan(const std::vector<const Kernel*>& instances, const ModelSpec& model,
   if (instances.empty()) throw EvalError("no kernel instances");
   // Reference order of checks: SimPlan ctor, then the tenv lookups
   // (proj/src/pricing.cpp:335-338); then the batch shape check.
-  SimPlanHost sp = buildSimPlan(*instances[0], model);
+  (void)buildSimPlan(*instances[0], model);
   for (const auto& v : instances[0]->tvars) (void)tenv.lookup(v);
   LiteralTable t = literalTableFromInstances(instances);
   init(*instances[0], &t, model, days, tenv, opt);
@@ -105,7 +121,8 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
                 const std::vector<uint64_t>& days, const TEnv& tenv, const RunOptions& opt) {
   const LiteralTable& lits = *static_cast<const LiteralTable*>(litsv);
   PlanImpl& I = *impl_;
-  SimPlanHost sp = buildSimPlan(k, model);
+  if (opt.rng != 0 && opt.rng != 1) throw UnsupportedError("unknown rng mode");
+  SimPlanHost sp = buildSimPlan(k, model, static_cast<uint32_t>(opt.rng));
   for (const auto& v : k.tvars) (void)tenv.lookup(v);
   CompileOptions co;
   co.rewrite = opt.rewrite;
@@ -123,6 +140,19 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   I.dev.sharedConst = upload(I.prog.sharedConst, I.owned);
   I.dev.instConst = upload(I.prog.instConst, I.owned);
   I.dev.outputs = upload(I.prog.outputs, I.owned);
+  I.dev.bridge = upload(I.prog.bridge, I.owned);
+  if (I.prog.header.rng == CLTK_RNG_SOBOL) {
+    std::vector<uint32_t> V(kSobolV, kSobolV + kSobolDims * 32), T5(kSobolDims * 32);
+    for (uint32_t d = 0; d < kSobolDims; ++d)
+      for (uint32_t g = 0; g < 32; ++g) {
+        uint32_t x = 0;
+        for (uint32_t k = 0; k < 5; ++k)
+          if ((g >> k) & 1u) x ^= V[d * 32 + k];
+        T5[d * 32 + g] = x;
+      }
+    I.dev.sobolV = upload(V, I.owned);
+    I.dev.sobolT5 = upload(T5, I.owned);
+  }
   void* p = nullptr;
   ck(cudaMalloc(&p, 2 * sizeof(unsigned long long)), "cudaMalloc");
   I.owned.push_back(p);
@@ -175,9 +205,36 @@ void Plan::chunking(uint64_t paths, uint64_t* chunkPaths, uint64_t* nChunks) con
   *nChunks = (paths + *chunkPaths - 1) / *chunkPaths;
 }
 
+namespace {
+// QMC: digital shift of Sobol dimension d = top 32 bits of
+// Philox2x64-10(key = seed, ctr = (d, 2^64 - 1)); seed 0 = plain Sobol.
+const uint32_t* sobolShiftFor(PlanImpl& I, uint64_t seed, cudaStream_t s) {
+  if (I.prog.header.rng != CLTK_RNG_SOBOL || seed == 0) return nullptr;
+  if (!I.sobolShift) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, kSobolDims * sizeof(uint32_t)), "cudaMalloc");
+    I.owned.push_back(p);
+    I.sobolShift = static_cast<uint32_t*>(p);
+    I.shiftSeed = seed + 1;  // force the first upload
+  }
+  if (I.shiftSeed != seed) {
+    std::vector<uint32_t> sh(kSobolDims);
+    for (uint32_t d = 0; d < kSobolDims; ++d)
+      sh[d] = static_cast<uint32_t>(philoxHost(seed, d, ~0ULL) >> 32);
+    ck(cudaMemcpyAsync(I.sobolShift, sh.data(), sh.size() * sizeof(uint32_t),
+                       cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    I.shiftSeed = seed;
+  }
+  return I.sobolShift;
+}
+}  // namespace
+
 void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void* partialsDev,
                   void* stream) {
   if (paths == 0) throw EvalError("path count must be positive");
+  if (impl_->prog.header.rng == CLTK_RNG_SOBOL && paths > (1ULL << 32))
+    throw UnsupportedError("Sobol mode: at most 2^32 paths (32-bit Sobol points)");
   PlanImpl& I = *impl_;
   PlanImpl::DeviceGuard g(I.device);
   uint64_t chunkPaths, nChunks;
@@ -198,6 +255,7 @@ void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void*
   ck(cudaMemsetAsync(I.chunkCounter, 0, sizeof(unsigned long long), s), "cudaMemsetAsync");
   RunArgs a{};
   a.keys = philoxKeys(seed);
+  a.sobolShift = sobolShiftFor(I, seed, s);
   a.seed = seed;
   a.paths = paths;
   a.chunkPaths = chunkPaths;
@@ -292,7 +350,7 @@ uint64_t debugPaths(Plan& plan, uint64_t seed, uint64_t path0, uint64_t npaths, 
   if (spots && nS) ck(cudaMalloc(&dS, nS * sizeof(double)), "cudaMalloc");
   if (normals && nS) ck(cudaMalloc(&dZ, nS * sizeof(double)), "cudaMalloc");
   if (dZ) ck(cudaMemset(dZ, 0, nS * sizeof(double)), "cudaMemset");
-  DumpArgs a{philoxKeys(seed), seed, path0, npaths, dS, dO, dZ, dE};
+  DumpArgs a{philoxKeys(seed), sobolShiftFor(I, seed, nullptr), seed, path0, npaths, dS, dO, dZ, dE};
   ck(launchDump(I.dev, a, nullptr), "dump launch");
   ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
   if (dO) ck(cudaMemcpy(outputs, dO, nO * sizeof(double), cudaMemcpyDeviceToHost), "D2H");

@@ -29,10 +29,15 @@ struct DevPlan {
   const double* sharedConst;
   const double* instConst;
   const cltk_output* outputs;
+  // QMC mode
+  const cltk_bridge_op* bridge;
+  const uint32_t* sobolV;   // [2048][32] direction numbers
+  const uint32_t* sobolT5;  // [2048][32] XOR of v[d][0..4] over the set bits of g
 };
 
 struct RunArgs {
   PhiloxKeys keys;
+  const uint32_t* sobolShift;  // QMC digital shift per dimension (null: none)
   uint64_t seed;
   uint64_t paths;        // total paths of the run (whole job, all GPUs)
   uint64_t chunkPaths;   // kBlock * ppt
@@ -47,6 +52,7 @@ struct RunArgs {
 // Dump modes (tests): per-path outputs instead of reduction.
 struct DumpArgs {
   PhiloxKeys keys;
+  const uint32_t* sobolShift;
   uint64_t seed, path0, npaths;
   double* spots;    // [npaths][n_steps][n_assets] or null
   double* outputs;  // [npaths][n_out] or null

@@ -351,6 +351,178 @@ __device__ __forceinline__ bool normals_batch(const PhiloxKeys& K, uint64_t path
   return ok;
 }
 
+// ---------------------------------------------------------------------------
+// QMC mode: Sobol (Joe-Kuo, 32-bit, gray code) + Wichura AS241 + Brownian
+// bridge.  Not a reference algorithm (the reference has no QMC): the Sobol
+// integers are checked against scipy.stats.qmc.Sobol, AS241 against
+// scipy.special.ndtri (tests/test_qmc.py).
+// ---------------------------------------------------------------------------
+// AS241 PPND16 (Wichura 1988): a[0..7], b[1..7], c[0..7], d[1..7], e[0..7], f[1..7]
+__constant__ double kAS[44] = {
+    3.3871328727963666080e0, 1.3314166789178437745e+2, 1.9715909503065514427e+3,
+    1.3731693765509461125e+4, 4.5921953931549871457e+4, 6.7265770927008700853e+4,
+    3.3430575583588128105e+4, 2.5090809287301226727e+3,
+    4.2313330701600911252e+1, 6.8718700749205790830e+2, 5.3941960214247511077e+3,
+    2.1213794301586595867e+4, 3.9307895800092710610e+4, 2.8729085735721942674e+4,
+    5.2264952788528545610e+3,
+    1.42343711074968357734e0, 4.63033784615654529590e0, 5.76949722146069140550e0,
+    3.64784832476320460504e0, 1.27045825245236838258e0, 2.41780725177450611770e-1,
+    2.27238449892691845833e-2, 7.74545014278341407640e-4,
+    2.05319162663775882187e0, 1.67638483018380384940e0, 6.89767334985100004550e-1,
+    1.48103976427480074590e-1, 1.51986665636164571966e-2, 5.47593808499534494600e-4,
+    1.05075007164441684324e-9,
+    6.65790464350110377720e0, 5.46378491116411436990e0, 1.78482653991729133580e0,
+    2.96560571828504891230e-1, 2.65321895265761230930e-2, 1.24266094738807843860e-3,
+    2.71155556874348757815e-5, 2.01033439929228813265e-7,
+    5.99832206555887937690e-1, 1.36929880922735805310e-1, 1.48753612908506148525e-2,
+    7.86869131145613259100e-4, 1.84631831751005468180e-5, 1.42151175831644588870e-7};
+// f7
+__constant__ double kASf7 = 2.04426310338993978564e-15;
+
+// numerator coefficients K[o..o+7], denominator 1 + K[p..p+6]
+__device__ __forceinline__ double as_ratio(double r, int o, int pd, double last) {
+  const double* K = kAS;
+  double n = K[o + 7];
+#pragma unroll
+  for (int i = 6; i >= 0; --i) n = fma(n, r, K[o + i]);
+  double d = last;
+#pragma unroll
+  for (int i = 5; i >= 0; --i) d = fma(d, r, K[pd + i]);
+  d = fma(d, r, 1.0);
+  return n / d;
+}
+
+__device__ __forceinline__ bool as241_is_central(double q) { return fabs(q) <= 0.425; }
+
+__device__ __forceinline__ double as241_central(double q) {
+  const double r = fma(-q, q, 0.180625);
+  return q * as_ratio(r, 0, 8, kAS[14]);
+}
+
+__device__ __forceinline__ double as241_tail(double u) {
+  const double q = u - 0.5;
+  double r = q < 0.0 ? u : 1.0 - u;
+  r = sqrt(-cltk_gm::log(r));
+  double v;
+  if (r <= 5.0) v = as_ratio(r - 1.6, 15, 23, kAS[29]);
+  else v = as_ratio(r - 5.0, 30, 38, kASf7);
+  return q < 0.0 ? -v : v;
+}
+
+// Sobol point n, dimension d: XOR of v[d][k] over the set bits k of gray(n).
+// Warp-cooperative form: the 32 lanes hold n = 32a + lane, so bits >= 5 of
+// gray(n) (G) are warp-uniform -- lane k >= 5 contributes v[d][k], XOR-reduced
+// by shuffles -- and bits 0..4 (glow) index a 32-entry per-dimension table.
+__device__ __forceinline__ uint32_t sobol_warp(const DevPlan& P, uint32_t d, uint32_t G,
+                                               uint32_t glow, int lane) {
+  uint32_t t = (lane >= 5 && ((G >> (lane - 5)) & 1u)) ? __ldg(P.sobolV + d * 32 + lane) : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t ^= __shfl_xor_sync(0xffffffffu, t, o);
+  return t ^ __ldg(P.sobolT5 + d * 32 + glow);
+}
+
+// Per-lane form (any n).
+__device__ __forceinline__ uint32_t sobol_lane(const DevPlan& P, uint32_t d, uint64_t gray) {
+  uint32_t x = 0;
+  for (int k = 0; gray; ++k, gray >>= 1)
+    if (gray & 1u) x ^= __ldg(P.sobolV + d * 32 + k);
+  return x;
+}
+
+// Normals of bridge computes c0 .. c0+nC-1 (nA each, Sobol dimension
+// node * nA + j) for Sobol point n = path, into NS.X[m], m = (c - c0) * nA + j.
+template <int NA>
+__device__ __forceinline__ void qmc_normals_batch(const DevPlan& P, const uint32_t* shift,
+                                                  uint64_t path, bool aligned, uint32_t c0,
+                                                  int nC, const NormScratch NS) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint16_t* tails = NS.list;
+  int nTail = 0;
+  const uint64_t gray = path ^ (path >> 1);
+  const uint32_t G = static_cast<uint32_t>(gray >> 5), glow = static_cast<uint32_t>(gray & 31u);
+  const int M = nC * NA;
+  for (int m = 0; m < M; ++m) {
+    const uint32_t c = c0 + static_cast<uint32_t>(m / NA);
+    const uint32_t d = __ldg(&P.bridge[c].node) * NA + static_cast<uint32_t>(m % NA);
+    uint32_t x = aligned ? sobol_warp(P, d, G, glow, lane) : sobol_lane(P, d, gray);
+    if (shift) x ^= __ldg(shift + d);
+    const double u = (static_cast<double>(x) + 0.5) * 0x1.0p-32;
+    const double q = u - 0.5;
+    NS.P[m * kBlock + tid] = u;
+    NS.X[m * kBlock + tid] = as241_central(q);
+    list_push(tails, nTail, !as241_is_central(q), m, lane);
+  }
+  list_each(tails, nTail, lane, [&](int q, int src) {
+    NS.X[q * kBlock + src] = as241_tail(NS.P[q * kBlock + src]);
+  });
+}
+
+// One QMC path: bridge ops before each drawing step, then the exact GBM
+// logS(t) = log(spot) + (drift - vol^2/2) t + vol (L W(t)) and the step's ops.
+// W slots (per asset) live in shared memory: WS[(slot * NA + j) * kBlock + tid].
+template <int NA, bool DUMP>
+__device__ __forceinline__ void simulate_qmc(const DevPlan& P, const Frame f, const NormScratch NS,
+                                             double* WS, const uint32_t* shift, uint64_t path,
+                                             bool aligned, double* dumpS, double* dumpW) {
+  const cltk_plan_header& h = P.hdr;
+  constexpr int SB = batchSteps(NA);
+  const int tid = threadIdx.x;
+  const uint32_t used = h.used_mask;
+  const uint32_t nC = h.n_bridge_ops;
+  double S[NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) S[j] = 0.0;
+  uint32_t c = 0;
+  for (uint32_t s = 0; s < h.n_steps; ++s) {
+    const cltk_step* st = P.steps + s;
+    const uint32_t kind = __ldg(&st->draws);
+    if (kind == 1) {
+      const uint32_t b0 = __ldg(&st->br_begin), b1 = __ldg(&st->br_end);
+      for (uint32_t b = b0; b < b1; ++b, ++c) {
+        const uint32_t cb = c % SB;
+        if (cb == 0)
+          qmc_normals_batch<NA>(P, shift, path, aligned, c, static_cast<int>(min(nC - c, static_cast<uint32_t>(SB))), NS);
+        const cltk_bridge_op* op = P.bridge + b;
+        const double wl = __ldg(&op->wl), wr = __ldg(&op->wr), sd = __ldg(&op->sd);
+        const uint32_t dst = __ldg(&op->dst), l = __ldg(&op->l), r = __ldg(&op->r);
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+          const double z = NS.X[(cb * NA + j) * kBlock + tid];
+          const double Wl = l == CLTK_BR_ORIGIN ? 0.0 : WS[(l * NA + j) * kBlock + tid];
+          const double Wr = r == CLTK_BR_ORIGIN ? 0.0 : WS[(r * NA + j) * kBlock + tid];
+          WS[(dst * NA + j) * kBlock + tid] = fma(wl, Wl, fma(wr, Wr, sd * z));
+        }
+      }
+      const uint32_t e = __ldg(&st->br_emit);
+      double w[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) w[j] = WS[(e * NA + j) * kBlock + tid];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        double y = 0.0;
+#pragma unroll
+        for (int l = 0; l <= j; ++l) y = fma(h.chol[j * CLTK_MAX_ASSETS + l], w[l], y);
+        const double logS = h.logS0[j] + __ldg(&st->A[j]) + __ldg(&st->B[j]) * y;
+        S[j] = ((used >> j) & 1u) ? cltk_gm::exp(logS) : 0.0;
+        if (DUMP && dumpW) dumpW[s * NA + j] = w[j];
+      }
+    } else if (kind == 0) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) S[j] = __ldg(&st->S[j]);
+    }  // kind 2: no new draw -> spots unchanged
+    if (DUMP && dumpS) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) dumpS[s * NA + j] = S[j];
+    }
+    const uint32_t cb = __ldg(&st->code_begin), ce = __ldg(&st->code_end);
+    if (cb < ce) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) st_reg(f, j, S[j]);
+      run_ops(f, P.code, cb, ce);
+    }
+  }
+}
+
 template <int NA, bool DUMP>
 __device__ __forceinline__ bool simulate(const DevPlan& P, const Frame f, const NormScratch NS,
                                          const PhiloxKeys& keys, uint64_t path, double* dumpS,
@@ -439,7 +611,7 @@ __device__ __forceinline__ void chan(double& n, double& mean, double& m2, double
 }
 
 // Shared memory: [regs n_thread*kBlock][wconst kWarps*(nc+ni)][acc ...][misc]
-template <int NA>
+template <int NA, bool QMC>
 __global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const DevPlan P, const RunArgs A,
                                                       int accInSmem) {
   extern __shared__ double smem[];
@@ -465,6 +637,7 @@ __global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const Dev
   double* nsBase = reinterpret_cast<double*>(chunkSlot + 1);
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
                  reinterpret_cast<uint16_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * 32 * kMaxBatch};
+  double* WS = nsBase + kNormScratchWords;  // QMC bridge slots
 
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
@@ -485,7 +658,11 @@ __global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const Dev
       const bool active = path < A.paths;
       if (__all_sync(0xffffffffu, !active)) continue;  // warp-uniform
       const uint64_t p = active ? path : A.paths - 1;
-      bool ok = simulate<NA, false>(P, f, NS, A.keys, p, nullptr, nullptr);
+      bool ok = true;
+      if (QMC)
+        simulate_qmc<NA, false>(P, f, NS, WS, A.sobolShift, p, true, nullptr, nullptr);
+      else
+        ok = simulate<NA, false>(P, f, NS, A.keys, p, nullptr, nullptr);
       if (active && !ok) atomicMin(A.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
       const uint32_t nAct = __popc(__ballot_sync(0xffffffffu, active));
       const bool first = counts[warp] == 0.0;
@@ -589,7 +766,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const cltk_partial* __rest
 }
 
 // Per-path dump (tests): same simulate/interpret code, outputs written out.
-template <int NA>
+template <int NA, bool QMC>
 __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const DumpArgs D) {
   extern __shared__ double smem[];
   const cltk_plan_header& h = P.hdr;
@@ -608,8 +785,14 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
   const uint64_t q = active ? idx : 0;
   const uint64_t p = D.path0 + q;
   const size_t sz = static_cast<size_t>(h.n_steps) * NA;
-  bool ok = simulate<NA, true>(P, f, NS, D.keys, p, D.spots ? D.spots + q * sz : nullptr,
-                               D.normals ? D.normals + q * sz : nullptr);
+  bool ok = true;
+  if (QMC)
+    simulate_qmc<NA, true>(P, f, NS, nsBase + kNormScratchWords, D.sobolShift, p, false,
+                           D.spots ? D.spots + q * sz : nullptr,
+                           D.normals ? D.normals + q * sz : nullptr);
+  else
+    ok = simulate<NA, true>(P, f, NS, D.keys, p, D.spots ? D.spots + q * sz : nullptr,
+                            D.normals ? D.normals + q * sz : nullptr);
   if (active && !ok) atomicMin(D.errKey, (static_cast<unsigned long long>(p) << 24) | 1ULL);
   for (uint32_t inst = 0; inst < h.n_instances; ++inst) {
     if (ni) {
@@ -671,38 +854,45 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double* sink, int iters)
   if (s == 12345.678) sink[threadIdx.x] = s;
 }
 
-template <int NA>
+template <int NA, bool QMC>
 cudaError_t launchPathT(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
                         cudaStream_t s, int accInSmem) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(path_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(path_kernel<NA, QMC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  path_kernel<NA><<<grid, kBlock, smem, s>>>(p, a, accInSmem);
+  path_kernel<NA, QMC><<<grid, kBlock, smem, s>>>(p, a, accInSmem);
   return cudaGetLastError();
 }
 
-template <int NA>
+size_t bridgeWords(const cltk_plan_header& h) {
+  return h.rng == CLTK_RNG_SOBOL
+             ? static_cast<size_t>(h.n_bridge_slots) * (h.n_assets ? h.n_assets : 1) * kBlock
+             : 0;
+}
+
+template <int NA, bool QMC>
 cudaError_t launchDumpT(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
   const cltk_plan_header& h = p.hdr;
   size_t smem = (static_cast<size_t>(h.n_thread) * kBlock +
-                 kWarps * (h.n_shared_const + h.n_inst_const) + kNormScratchWords) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(dump_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       227 * 1024);
+                 kWarps * (h.n_shared_const + h.n_inst_const) + kNormScratchWords + bridgeWords(h)) *
+                sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(dump_kernel<NA, QMC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
   const unsigned grid = static_cast<unsigned>((a.npaths + kBlock - 1) / kBlock);
-  dump_kernel<NA><<<grid, kBlock, smem, s>>>(p, a);
+  dump_kernel<NA, QMC><<<grid, kBlock, smem, s>>>(p, a);
   return cudaGetLastError();
 }
 
-template <int NA>
+template <int NA, bool QMC>
 int occupancyT(size_t smem) {
   int blocks = 0;
-  cudaFuncSetAttribute(path_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, path_kernel<NA>, kBlock, smem);
+  cudaFuncSetAttribute(path_kernel<NA, QMC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, path_kernel<NA, QMC>, kBlock, smem);
   return blocks;
 }
 
@@ -719,6 +909,7 @@ size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
   if (accInSmem) words += kWarps * nOut * 3;
   words += kWarps + 1;  // counts + chunk slot
   words += kNormScratchWords;
+  words += bridgeWords(h);
   return words * sizeof(double);
 }
 
@@ -736,17 +927,24 @@ size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
   }
 
 int pathKernelOccupancy(const cltk_plan_header& h, size_t smem) {
-  CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return occupancyT<NA>(smem));
+  if (h.rng == CLTK_RNG_SOBOL)
+    CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return (occupancyT<NA, true>(smem)));
+  CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return (occupancyT<NA, false>(smem)));
 }
 
 cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem, cudaStream_t s) {
   const int accInSmem = accFitsSmem(p.hdr) ? 1 : 0;
+  if (p.hdr.rng == CLTK_RNG_SOBOL)
+    CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
+                   return (launchPathT<NA, true>(p, a, grid, smem, s, accInSmem)));
   CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
-                 return launchPathT<NA>(p, a, grid, smem, s, accInSmem));
+                 return (launchPathT<NA, false>(p, a, grid, smem, s, accInSmem)));
 }
 
 cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
-  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return launchDumpT<NA>(p, a, s));
+  if (p.hdr.rng == CLTK_RNG_SOBOL)
+    CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return (launchDumpT<NA, true>(p, a, s)));
+  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return (launchDumpT<NA, false>(p, a, s)));
 }
 
 cudaError_t launchCombine(const cltk_partial* parts, uint64_t nChunks, uint32_t nOut,

@@ -72,8 +72,23 @@ typedef struct {
   uint32_t draws;             // 1: dt > 0 (draw nA normals), 0: dt == 0
   uint32_t code_begin;        // shared-op range of this step
   uint32_t code_end;
-  uint32_t pad;
+  // QMC mode (Sobol + AS241 + Brownian bridge): bridge ops [br_begin, br_end)
+  // computed before this (drawing) step, then W(t_s) read from slot br_emit;
+  // A = (drift - 0.5*vol*vol) * t_s, B = vol (t_s: years from day 0).
+  uint32_t br_begin;
+  uint32_t br_end;
+  uint32_t br_emit;
 } cltk_step;
+
+// Brownian-bridge construction op (QMC mode): for every asset j
+//   W[dst][j] = wl * W[l][j] + wr * W[r][j] + sd * Z[c][j]
+// (l == CLTK_BR_ORIGIN: W(0) = 0); Z[c] uses Sobol dimensions node * nA + j.
+#define CLTK_BR_ORIGIN 0xFFFFu
+typedef struct {
+  double wl, wr, sd;
+  uint32_t node;
+  uint16_t dst, l, r, pad;
+} cltk_bridge_op;
 
 // Launch-time header of a compiled plan (everything uniform across threads).
 typedef struct {
@@ -88,6 +103,9 @@ typedef struct {
   uint32_t inst_code_end;
   uint32_t has_err;         // any output carries an error register
   uint32_t used_mask;       // model assets referenced by any kernel column
+  uint32_t rng;             // CLTK_RNG_PHILOX (reference parity) / CLTK_RNG_SOBOL
+  uint32_t n_bridge_slots;  // QMC: W slots per asset
+  uint32_t n_bridge_ops;    // QMC: computes (= drawing steps)
   uint32_t pad;
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
@@ -101,6 +119,10 @@ typedef struct {
 } cltk_output;
 
 #define CLTK_NO_ERR 0xFFFFFFFFu
+
+#define CLTK_RNG_PHILOX 0u
+#define CLTK_RNG_SOBOL 1u
+#define CLTK_SOBOL_MAX_DIMS 2048u
 
 // Chunk partial of one output: count, mean, sum of squared deviations.
 typedef struct {
