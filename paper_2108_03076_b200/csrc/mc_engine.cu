@@ -635,9 +635,15 @@ __global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const Dev
   unsigned long long* chunkSlot =
       reinterpret_cast<unsigned long long*>(counts + kWarps);
   double* nsBase = reinterpret_cast<double*>(chunkSlot + 1);
+  // [X][P][Y | QMC bridge slots][work lists]: QMC never uses Y, its bridge
+  // slots start there and may extend beyond it
+  const size_t yWords = QMC ? max(static_cast<size_t>(kMaxBatch) * kBlock,
+                                  static_cast<size_t>(h.n_bridge_slots) * NA * kBlock)
+                            : static_cast<size_t>(kMaxBatch) * kBlock;
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
-                 reinterpret_cast<uint16_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * 32 * kMaxBatch};
-  double* WS = nsBase + kNormScratchWords;  // QMC bridge slots
+                 reinterpret_cast<uint16_t*>(nsBase + 2 * kMaxBatch * kBlock + yWords) +
+                     warp * 3 * 32 * kMaxBatch};
+  double* WS = nsBase + 2 * kMaxBatch * kBlock;
 
   for (uint32_t i = lane; i < nc; i += 32) wconst[i] = __ldg(P.sharedConst + i);
   __syncwarp();
@@ -778,8 +784,12 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
   __syncwarp();
   Frame f{smem_addr(smem + tid), smem_addr(wconst) - h.n_thread * 8u, h.n_thread};
   double* nsBase = smem + static_cast<size_t>(h.n_thread) * kBlock + kWarps * (nc + ni);
+  const size_t yWords = QMC ? max(static_cast<size_t>(kMaxBatch) * kBlock,
+                                  static_cast<size_t>(h.n_bridge_slots) * NA * kBlock)
+                            : static_cast<size_t>(kMaxBatch) * kBlock;
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
-                 reinterpret_cast<uint16_t*>(nsBase + 3 * kMaxBatch * kBlock) + warp * 3 * 32 * kMaxBatch};
+                 reinterpret_cast<uint16_t*>(nsBase + 2 * kMaxBatch * kBlock + yWords) +
+                     warp * 3 * 32 * kMaxBatch};
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kBlock + tid;
   const bool active = idx < D.npaths;
   const uint64_t q = active ? idx : 0;
@@ -787,7 +797,7 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
   const size_t sz = static_cast<size_t>(h.n_steps) * NA;
   bool ok = true;
   if (QMC)
-    simulate_qmc<NA, true>(P, f, NS, nsBase + kNormScratchWords, D.sobolShift, p, false,
+    simulate_qmc<NA, true>(P, f, NS, nsBase + 2 * kMaxBatch * kBlock, D.sobolShift, p, false,
                            D.spots ? D.spots + q * sz : nullptr,
                            D.normals ? D.normals + q * sz : nullptr);
   else
@@ -868,10 +878,13 @@ cudaError_t launchPathT(const DevPlan& p, const RunArgs& a, int grid, size_t sme
   return cudaGetLastError();
 }
 
+// QMC bridge slots overlap the (unused) Y slots and the work lists after
+// them; only the excess needs extra shared memory.
 size_t bridgeWords(const cltk_plan_header& h) {
-  return h.rng == CLTK_RNG_SOBOL
-             ? static_cast<size_t>(h.n_bridge_slots) * (h.n_assets ? h.n_assets : 1) * kBlock
-             : 0;
+  if (h.rng != CLTK_RNG_SOBOL) return 0;
+  const size_t need = static_cast<size_t>(h.n_bridge_slots) * (h.n_assets ? h.n_assets : 1) * kBlock;
+  const size_t have = kMaxBatch * kBlock;  // the Y slots
+  return need > have ? need - have : 0;
 }
 
 template <int NA, bool QMC>
