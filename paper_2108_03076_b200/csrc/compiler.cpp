@@ -1122,9 +1122,39 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
     if (d.op == OP_EDIVZ) c = static_cast<uint32_t>(d.bits);
     P.code.push_back(cltk_encode(d.op, dst, a, b, c));
   }
+  // Device stream: runs of one vectorisable opcode get a VEC header so the
+  // device executes them in one tight loop.  The listing keeps the plain ops.
+  auto vecable = [](uint32_t op) {
+    return op == OP_MIN || op == OP_MAX || op == OP_ADD || op == OP_SUB || op == OP_MUL ||
+           op == OP_LT || op == OP_LEQ || op == OP_OR || op == OP_AND;
+  };
+  std::vector<uint32_t> packedAt(P.code.size() + 1, 0);
+  auto pack = [&](uint32_t lo, uint32_t hi) {
+    uint32_t i = lo;
+    while (i < hi) {
+      const uint32_t op = static_cast<uint32_t>(P.code[i] & 0xff);
+      uint32_t j = i + 1;
+      while (j < hi && static_cast<uint32_t>(P.code[j] & 0xff) == op && j - i < 0x3fff) ++j;
+      if (vecable(op) && j - i >= 2) {
+        P.packed.push_back(cltk_encode(OP_VEC, j - i, op, 0, 0));
+        for (uint32_t k = i; k < j; ++k) P.packed.push_back(P.code[k]);
+      } else {
+        for (uint32_t k = i; k < j; ++k) P.packed.push_back(P.code[k]);
+      }
+      i = j;
+    }
+  };
+  std::vector<uint32_t> pBegin(nSteps + 1);
   for (uint32_t s = 0; s < nSteps; ++s) {
-    P.steps[s].code_begin = stepBegin[s];
-    P.steps[s].code_end = stepBegin[s + 1];
+    pBegin[s] = static_cast<uint32_t>(P.packed.size());
+    pack(stepBegin[s], stepBegin[s + 1]);
+  }
+  pBegin[nSteps] = static_cast<uint32_t>(P.packed.size());
+  const uint32_t pEndBegin = static_cast<uint32_t>(P.packed.size());
+  pack(endBegin, static_cast<uint32_t>(P.code.size()));
+  for (uint32_t s = 0; s < nSteps; ++s) {
+    P.steps[s].code_begin = pBegin[s];
+    P.steps[s].code_end = pBegin[s + 1];
   }
   uint32_t hasErr = 0;
   for (std::size_t o = 0; o < outs.size(); ++o) {
@@ -1150,8 +1180,8 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   h.n_inst_const = nInstC;
   h.n_instances = static_cast<uint32_t>(nInst);
   h.n_days = static_cast<uint32_t>(days.size());
-  h.inst_code_begin = endBegin;
-  h.inst_code_end = static_cast<uint32_t>(linear.size());
+  h.inst_code_begin = pEndBegin;
+  h.inst_code_end = static_cast<uint32_t>(P.packed.size());
   h.has_err = hasErr;
   h.used_mask = plan.usedMask;
   h.rng = plan.rng;
@@ -1181,7 +1211,8 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
       Bv.push_back(s.B[j]);
       Sv.push_back(s.S[j]);
     }
-    st.push_back({{"kind", s.draws}, {"begin", s.code_begin}, {"end", s.code_end},
+    const std::size_t si = st.size();
+    st.push_back({{"kind", s.draws}, {"begin", stepBegin[si]}, {"end", stepBegin[si + 1]},
                   {"A", A}, {"B", Bv}, {"S", Sv}, {"br", {s.br_begin, s.br_end, s.br_emit}}});
   }
   L["steps"] = st;
@@ -1208,7 +1239,8 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   L["n_shared_const"] = h.n_shared_const;
   L["n_inst_const"] = nInstC;
   L["n_instances"] = nInst;
-  L["inst_code"] = {endBegin, h.inst_code_end};
+  L["inst_code"] = {endBegin, static_cast<uint32_t>(linear.size())};
+  L["packed_words"] = P.packed.size();
   L["kernel_nodes"] = P.kernelNodes;
   L["dag_nodes"] = P.dagNodes;
   Json ch = Json::array();

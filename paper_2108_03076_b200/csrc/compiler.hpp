@@ -56,6 +56,7 @@ enum : uint32_t { STEP_CONST_S = 0, STEP_DRAW = 1, STEP_EXP_ONLY = 2 };
 struct CompiledProgram {
   std::vector<cltk_bridge_op> bridge;  // QMC mode
   std::vector<uint64_t> code;          // shared ops (step-ordered) then instance ops
+  std::vector<uint64_t> packed;        // device stream: code with VEC run headers
   std::vector<cltk_step> steps;        // simulation constants + shared-op ranges
   std::vector<double> sharedConst;     // bit patterns for B/I/E constants
   std::vector<double> instConst;       // [n_instances][n_inst_const]

@@ -136,7 +136,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   ck(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, dev), "attr");
   I.dev.hdr = I.prog.header;
   I.dev.steps = upload(I.prog.steps, I.owned);
-  I.dev.code = upload(I.prog.code, I.owned);
+  I.dev.code = upload(I.prog.packed, I.owned);
   I.dev.sharedConst = upload(I.prog.sharedConst, I.owned);
   I.dev.instConst = upload(I.prog.instConst, I.owned);
   I.dev.outputs = upload(I.prog.outputs, I.owned);

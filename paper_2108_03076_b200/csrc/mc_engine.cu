@@ -191,56 +191,77 @@ __device__ __forceinline__ void st_reg(const Frame f, uint32_t idx, double v) {
 __device__ __forceinline__ int64_t bits_of(double v) { return __double_as_longlong(v); }
 __device__ __forceinline__ double of_bits(int64_t v) { return __longlong_as_double(v); }
 
+#define CLTK_VEC_LOOP(EXPR)                                                  \
+  for (uint32_t i = 0; i < n; ++i) {                                         \
+    const uint64_t u = __ldg(code + pc + i);                                 \
+    const double va = ld(f, static_cast<uint32_t>(u >> 22) & 0x3fff);       \
+    const double vb = ld(f, static_cast<uint32_t>(u >> 36) & 0x3fff);       \
+    st_reg(f, static_cast<uint32_t>(u >> 8) & 0x3fff, (EXPR));              \
+  }
+
 __device__ __noinline__ void run_ops(const Frame f, const uint64_t* __restrict__ code,
                                      uint32_t begin, uint32_t end) {
-  for (uint32_t pc = begin; pc < end; ++pc) {
+  for (uint32_t pc = begin; pc < end;) {
     const uint64_t w = __ldg(code + pc);
     const uint32_t op = static_cast<uint32_t>(w & 0xff);
+    ++pc;
+    if (op == OP_VEC) {  // a run of one opcode: one dispatch, tight loop
+      const uint32_t n = static_cast<uint32_t>(w >> 8) & 0x3fff;
+      switch (static_cast<uint32_t>(w >> 22) & 0x3fff) {
+        case OP_MIN: CLTK_VEC_LOOP(fmin(va, vb)) break;
+        case OP_MAX: CLTK_VEC_LOOP(fmax(va, vb)) break;
+        case OP_ADD: CLTK_VEC_LOOP(__dadd_rn(va, vb)) break;
+        case OP_SUB: CLTK_VEC_LOOP(__dsub_rn(va, vb)) break;
+        case OP_MUL: CLTK_VEC_LOOP(__dmul_rn(va, vb)) break;
+        case OP_LT: CLTK_VEC_LOOP(va < vb ? 1.0 : 0.0) break;
+        case OP_LEQ: CLTK_VEC_LOOP(va <= vb ? 1.0 : 0.0) break;
+        case OP_OR: CLTK_VEC_LOOP((va != 0.0 || vb != 0.0) ? 1.0 : 0.0) break;
+        case OP_AND: CLTK_VEC_LOOP((va != 0.0 && vb != 0.0) ? 1.0 : 0.0) break;
+        default: break;
+      }
+      pc += n;
+      continue;
+    }
     const uint32_t d = static_cast<uint32_t>(w >> 8) & 0x3fff;
     const double va = ld(f, static_cast<uint32_t>(w >> 22) & 0x3fff);
     const double vb = ld(f, static_cast<uint32_t>(w >> 36) & 0x3fff);
     double r;
-    // the running min/max of barrier monitoring first, then the rest
-    if (op == OP_MIN) {
-      r = fmin(va, vb);
-    } else if (op == OP_MAX) {
-      r = fmax(va, vb);
-    } else {
-      switch (op) {
-        case OP_MOV: r = va; break;
-        case OP_NEG: r = -va; break;
-        case OP_NOT: r = va == 0.0 ? 1.0 : 0.0; break;
-        case OP_ADD: r = __dadd_rn(va, vb); break;
-        case OP_SUB: r = __dsub_rn(va, vb); break;
-        case OP_MUL: r = __dmul_rn(va, vb); break;
-        case OP_DIV: r = __ddiv_rn(va, vb); break;
-        case OP_LT: r = va < vb ? 1.0 : 0.0; break;
-        case OP_LEQ: r = va <= vb ? 1.0 : 0.0; break;
-        case OP_EQ: r = va == vb ? 1.0 : 0.0; break;
-        case OP_AND: r = (va != 0.0 && vb != 0.0) ? 1.0 : 0.0; break;
-        case OP_OR: r = (va != 0.0 || vb != 0.0) ? 1.0 : 0.0; break;
-        case OP_SEL: r = va != 0.0 ? vb : ld(f, static_cast<uint32_t>(w >> 50) & 0x3fff); break;
-        case OP_IADD:
-          r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) +
-                                           static_cast<uint64_t>(bits_of(vb))));
-          break;
-        case OP_ISUB:
-          r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) -
-                                           static_cast<uint64_t>(bits_of(vb))));
-          break;
-        case OP_ILT: r = bits_of(va) < bits_of(vb) ? 1.0 : 0.0; break;
-        case OP_ILEQ: r = bits_of(va) <= bits_of(vb) ? 1.0 : 0.0; break;
-        case OP_IEQ: r = bits_of(va) == bits_of(vb) ? 1.0 : 0.0; break;
-        case OP_MINP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                   : fmin(va, vb);
-          break;
-        case OP_MAXP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                   : fmax(va, vb);
-          break;
-        case OP_EFIRST: r = bits_of(va) != 0 ? va : vb; break;
-        case OP_EDIVZ: r = va == 0.0 ? of_bits(static_cast<int64_t>(w >> 50)) : 0.0; break;
-        default: r = 0.0; break;
-      }
+    switch (op) {
+      case OP_MIN: r = fmin(va, vb); break;
+      case OP_MAX: r = fmax(va, vb); break;
+      case OP_MOV: r = va; break;
+      case OP_NEG: r = -va; break;
+      case OP_NOT: r = va == 0.0 ? 1.0 : 0.0; break;
+      case OP_ADD: r = __dadd_rn(va, vb); break;
+      case OP_SUB: r = __dsub_rn(va, vb); break;
+      case OP_MUL: r = __dmul_rn(va, vb); break;
+      case OP_DIV: r = __ddiv_rn(va, vb); break;
+      case OP_LT: r = va < vb ? 1.0 : 0.0; break;
+      case OP_LEQ: r = va <= vb ? 1.0 : 0.0; break;
+      case OP_EQ: r = va == vb ? 1.0 : 0.0; break;
+      case OP_AND: r = (va != 0.0 && vb != 0.0) ? 1.0 : 0.0; break;
+      case OP_OR: r = (va != 0.0 || vb != 0.0) ? 1.0 : 0.0; break;
+      case OP_SEL: r = va != 0.0 ? vb : ld(f, static_cast<uint32_t>(w >> 50) & 0x3fff); break;
+      case OP_IADD:
+        r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) +
+                                         static_cast<uint64_t>(bits_of(vb))));
+        break;
+      case OP_ISUB:
+        r = of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(va)) -
+                                         static_cast<uint64_t>(bits_of(vb))));
+        break;
+      case OP_ILT: r = bits_of(va) < bits_of(vb) ? 1.0 : 0.0; break;
+      case OP_ILEQ: r = bits_of(va) <= bits_of(vb) ? 1.0 : 0.0; break;
+      case OP_IEQ: r = bits_of(va) == bits_of(vb) ? 1.0 : 0.0; break;
+      case OP_MINP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                 : fmin(va, vb);
+        break;
+      case OP_MAXP: r = (isnan(va) || isnan(vb)) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                 : fmax(va, vb);
+        break;
+      case OP_EFIRST: r = bits_of(va) != 0 ? va : vb; break;
+      case OP_EDIVZ: r = va == 0.0 ? of_bits(static_cast<int64_t>(w >> 50)) : 0.0; break;
+      default: r = 0.0; break;
     }
     st_reg(f, d, r);
   }

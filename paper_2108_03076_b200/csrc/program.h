@@ -53,7 +53,10 @@ enum cltk_opcode : uint32_t {
   OP_MAXP,     // R: NaN-propagating max
   OP_EFIRST,   // E: d = a != 0 ? a : b
   OP_EDIVZ,    // E: d = (a == 0.0) ? c(field) : 0   (c is an immediate site id)
-  OP_COUNT
+  OP_COUNT,
+  // Run header: the next d(field) words are ops of opcode a(field), executed
+  // by one tight loop (no per-op dispatch).  Emitted for runs >= 2.
+  OP_VEC = 63
 };
 
 // 64-bit instruction: op | d<<8 | a<<22 | b<<36 | c<<50
