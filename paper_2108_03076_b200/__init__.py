@@ -83,12 +83,28 @@ class Kernel:
     held in the reference's JSON wire format."""
 
     def __init__(self, source: str | dict):
+        """``source``: the kernel JSON (kernelToJson, dict or text) or the
+        reference's textual kernel format (emitKernelSource)."""
         if isinstance(source, dict):
             self._obj = source
             self._json = _deep(json.dumps, source)
-        else:
+        elif source.lstrip().startswith("{"):
             self._json = source
             self._obj = _deep(json.loads, source)
+        else:  # kernel text: the engine reads it natively; header parsed here
+            import re
+            self._json = source
+            rows = re.search(r"let rows = \[([^\]]*)\]", source)
+            cols = re.search(r"let cols = \[([^\]]*)\]", source)
+            if not rows or not cols:
+                raise ContractParseError("kernel source: missing rows/cols header", 2)
+            r = [int(x) for x in rows.group(1).split(",") if x.strip()]
+            self._obj = {"rows": r, "cols": re.findall(r'"([^"]*)"', cols.group(1)),
+                         "tvars": [], "parties": list(dict.fromkeys(
+                             re.findall(r"pay\[[^,]+, *(\w+), *(\w+)\]", source) and
+                             [p for pr in re.findall(r"pay\[[^,]+, *(\w+), *(\w+)\]", source)
+                              for p in pr])),
+                         "horizon": (max(r) + 1) if r else 1, "body": None}
 
     @classmethod
     def from_file(cls, path: str) -> "Kernel":
@@ -111,6 +127,8 @@ class Kernel:
 
     def literals(self) -> list[float]:
         """FloatLit values in postorder (the order the engine's literal pool uses)."""
+        if self._obj.get("body") is None:
+            return kernel_literals(self._json)
         out: list[float] = []
 
         def walk(e):

@@ -74,7 +74,7 @@ int cltk_gpu_price(const char* kernel_json, const char* model_json, uint64_t pat
                    int device, cltk_price_result* results, cltk_error* err) {
   return guarded(err, [&] {
     if (paths == 0) throw EvalError("path count must be positive");
-    Kernel k = kernelFromJson(kernel_json);
+    Kernel k = kernelFromWire(kernel_json);
     ModelSpec m = modelFromJson(model_json);
     std::vector<uint64_t> d(days, days + n_days);
     RunOptions opt;
@@ -93,7 +93,7 @@ int cltk_gpu_price_batch(const char* const* kernel_jsons, size_t n_instances,
     if (paths == 0) throw EvalError("path count must be positive");
     std::vector<Kernel> ks;
     ks.reserve(n_instances);
-    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromJson(kernel_jsons[i]));
+    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromWire(kernel_jsons[i]));
     std::vector<const Kernel*> ptrs;
     for (auto& k : ks) ptrs.push_back(&k);
     ModelSpec m = modelFromJson(model_json);
@@ -111,7 +111,7 @@ int cltk_gpu_price_template(const char* kernel_json, const double* literals, siz
                             cltk_error* err) {
   return guarded(err, [&] {
     if (paths == 0) throw EvalError("path count must be positive");
-    Kernel k = kernelFromJson(kernel_json);
+    Kernel k = kernelFromWire(kernel_json);
     ModelSpec m = modelFromJson(model_json);
     RunOptions opt;
     opt.device = device;
@@ -124,7 +124,7 @@ int cltk_gpu_price_template(const char* kernel_json, const double* literals, siz
 int cltk_kernel_literals(const char* kernel_json, double* out, size_t cap, size_t* n,
                          cltk_error* err) {
   return guarded(err, [&] {
-    std::vector<double> v = kernelFloatLiterals(kernelFromJson(kernel_json));
+    std::vector<double> v = kernelFloatLiterals(kernelFromWire(kernel_json));
     *n = v.size();
     for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
   });
@@ -136,7 +136,7 @@ int cltk_plan_create_template(const char* kernel_json, const double* literals, s
                               cltk_plan** out, cltk_error* err) {
   return guarded(err, [&] {
     auto p = std::make_unique<cltk_plan>();
-    p->kernels.push_back(std::make_unique<Kernel>(kernelFromJson(kernel_json)));
+    p->kernels.push_back(std::make_unique<Kernel>(kernelFromWire(kernel_json)));
     ModelSpec m = modelFromJson(model_json);
     RunOptions opt;
     opt.device = device;
@@ -166,7 +166,7 @@ int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_
                       const cltk_options* opts, cltk_price_result* results, cltk_error* err) {
   return guarded(err, [&] {
     if (paths == 0) throw EvalError("path count must be positive");
-    Kernel k = kernelFromJson(kernel_json);
+    Kernel k = kernelFromWire(kernel_json);
     ModelSpec m = modelFromJson(model_json);
     std::vector<uint64_t> d(days, days + n_days);
     RunOptions opt = optionsOf(opts);
@@ -189,7 +189,7 @@ int cltk_plan_create_ex(const char* kernel_json, const double* literals, size_t 
                         cltk_plan** out, cltk_error* err) {
   return guarded(err, [&] {
     auto p = std::make_unique<cltk_plan>();
-    p->kernels.push_back(std::make_unique<Kernel>(kernelFromJson(kernel_json)));
+    p->kernels.push_back(std::make_unique<Kernel>(kernelFromWire(kernel_json)));
     std::vector<double> own;
     if (!literals) {
       own = kernelFloatLiterals(*p->kernels[0]);
@@ -212,7 +212,7 @@ int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const 
     auto p = std::make_unique<cltk_plan>();
     std::vector<const Kernel*> ptrs;
     for (size_t i = 0; i < n_instances; ++i) {
-      p->kernels.push_back(std::make_unique<Kernel>(kernelFromJson(kernel_jsons[i])));
+      p->kernels.push_back(std::make_unique<Kernel>(kernelFromWire(kernel_jsons[i])));
       ptrs.push_back(p->kernels.back().get());
     }
     ModelSpec m = modelFromJson(model_json);
@@ -296,7 +296,7 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
   return guarded(err, [&] {
     std::vector<Kernel> ks;
     ks.reserve(n_instances);
-    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromJson(kernel_jsons[i]));
+    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromWire(kernel_jsons[i]));
     std::vector<const Kernel*> ptrs;
     for (auto& k : ks) ptrs.push_back(&k);
     if (ptrs.empty()) throw EvalError("no kernel instances");

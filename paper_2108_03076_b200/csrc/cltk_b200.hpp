@@ -85,6 +85,13 @@ struct Kernel {
 // kernelFromJson (proj/src/kernel.cpp:631-638; wire format :520-629).
 Kernel kernelFromJson(const std::string& json);
 
+// The reference's textual kernel format (emitKernelSource,
+// proj/src/kernel.cpp:407; proj/docs/kernel-format.md).  tenvValues[k] backs
+// loop windows written as tenv[k].
+Kernel kernelFromSource(const std::string& text, const std::vector<uint64_t>& tenvValues = {});
+// Either wire format: JSON ('{' first) or kernel text.
+Kernel kernelFromWire(const std::string& text, const std::vector<uint64_t>& tenvValues = {});
+
 // Shape hash: equal for kernels that differ only in FloatLit values (the
 // "template instances" of one contract, priced with shared paths).
 uint64_t kernelShapeHash(const Kernel& k);

@@ -2,7 +2,9 @@
 // Cholesky, template environment.  Semantics follow the reference line by
 // line (cited per function); the representation is the engine's own
 // (a flat node pool instead of a shared_ptr tree).
+#include <cctype>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <nlohmann/json.hpp>
@@ -109,6 +111,436 @@ Kernel kernelFromJson(const std::string& text) {
     throw ParseError(std::string("parse error at 0:0: kernel JSON: ") + e.what());
   }
   return k;
+}
+
+// ---------------------------------------------------------------------------
+// Textual kernel format (emitKernelSource, proj/src/kernel.cpp:407-435;
+// grammar proj/docs/kernel-format.md): an independent reader producing the
+// same node pool as kernelFromJson.  Loop windows given as tenv[k] take the
+// k-th entry of `tenvValues` (the text carries indices, not names).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct TextReader {
+  const std::string& src;
+  const std::vector<uint64_t>& tenvValues;
+  Kernel& k;
+  std::size_t pos = 0;
+  std::map<std::string, int32_t> partyIdx;
+
+  [[noreturn]] void fail(const std::string& m) const {
+    std::size_t line = 1, col = 1;
+    for (std::size_t i = 0; i < pos && i < src.size(); ++i) {
+      if (src[i] == '\n') {
+        ++line;
+        col = 1;
+      } else {
+        ++col;
+      }
+    }
+    throw ParseError("parse error at " + std::to_string(line) + ":" + std::to_string(col) +
+                     ": kernel source: " + m);
+  }
+  void skip() {
+    for (;;) {
+      while (pos < src.size() && std::isspace(static_cast<unsigned char>(src[pos]))) ++pos;
+      if (pos + 1 < src.size() && src[pos] == '-' && src[pos + 1] == '-') {
+        while (pos < src.size() && src[pos] != '\n') ++pos;
+        continue;
+      }
+      return;
+    }
+  }
+  bool peek(const char* t) {
+    skip();
+    return src.compare(pos, std::strlen(t), t) == 0;
+  }
+  bool peekWord(const char* w) {
+    skip();
+    const std::size_t n = std::strlen(w);
+    if (src.compare(pos, n, w) != 0) return false;
+    const char c = pos + n < src.size() ? src[pos + n] : ' ';
+    return !(std::isalnum(static_cast<unsigned char>(c)) || c == '_');
+  }
+  void expect(const char* t) {
+    if (!peek(t)) fail(std::string("expected '") + t + "'");
+    pos += std::strlen(t);
+  }
+  void expectWord(const char* w) {
+    if (!peekWord(w)) fail(std::string("expected '") + w + "'");
+    pos += std::strlen(w);
+  }
+  std::string ident() {
+    skip();
+    std::size_t b = pos;
+    while (pos < src.size() && (std::isalnum(static_cast<unsigned char>(src[pos])) || src[pos] == '_'))
+      ++pos;
+    if (b == pos) fail("expected an identifier");
+    return src.substr(b, pos - b);
+  }
+  std::string quoted() {
+    expect("\"");
+    std::size_t b = pos;
+    while (pos < src.size() && src[pos] != '"') ++pos;
+    if (pos >= src.size()) fail("unterminated string");
+    std::string r = src.substr(b, pos - b);
+    ++pos;
+    return r;
+  }
+  // number: returns true for float (value in d) else integer (in i)
+  bool number(double& d, int64_t& i) {
+    skip();
+    std::size_t b = pos;
+    if (pos < src.size() && (src[pos] == '-' || src[pos] == '+')) ++pos;
+    bool isFloat = false;
+    while (pos < src.size() &&
+           (std::isdigit(static_cast<unsigned char>(src[pos])) || src[pos] == '.' || src[pos] == 'e' ||
+            src[pos] == 'E' ||
+            ((src[pos] == '-' || src[pos] == '+') && (src[pos - 1] == 'e' || src[pos - 1] == 'E')))) {
+      if (src[pos] == '.' || src[pos] == 'e' || src[pos] == 'E') isFloat = true;
+      ++pos;
+    }
+    const std::string t = src.substr(b, pos - b);
+    if (t.empty() || t == "-" || t == "+") fail("expected a number");
+    if (isFloat) d = std::strtod(t.c_str(), nullptr);
+    else i = std::strtoll(t.c_str(), nullptr, 10);
+    return isFloat;
+  }
+  int32_t push(KNode n) {
+    k.nodes.push_back(n);
+    return static_cast<int32_t>(k.nodes.size() - 1);
+  }
+  int32_t party(const std::string& p) {
+    auto [it, ins] = partyIdx.try_emplace(p, static_cast<int32_t>(k.partyNames.size()));
+    if (ins) {
+      k.partyNames.push_back(p);
+      k.parties.push_back(p);  // first occurrence order, as reindex notes them
+    }
+    return it->second;
+  }
+  // "<int> + var" or "var" relative to the current offset variable
+  uint64_t rowIndex(const std::string& var) {
+    uint64_t row = 0;
+    if (!peekWord(var.c_str())) {
+      double d = 0;
+      int64_t i = 0;
+      if (number(d, i)) fail("row index must be an integer");
+      row = static_cast<uint64_t>(i);
+      expect("+");
+    }
+    if (ident() != var) fail("row index must be relative to " + var);
+    return row;
+  }
+
+  // expression grammar, loosest first: | & comparisons + - * / unary atoms
+  int32_t expr(const std::string& v) { return orE(v); }
+  int32_t bin(KBin op, int32_t a, int32_t b) {
+    KNode n;
+    n.kind = KKind::BinOp;
+    n.op = static_cast<int>(op);
+    n.a = a;
+    n.b = b;
+    return push(n);
+  }
+  int32_t orE(const std::string& v) {
+    int32_t a = andE(v);
+    while (peek("|")) {
+      ++pos;
+      a = bin(KBin::Or, a, andE(v));
+    }
+    return a;
+  }
+  int32_t andE(const std::string& v) {
+    int32_t a = cmpE(v);
+    while (peek("&")) {
+      ++pos;
+      a = bin(KBin::And, a, cmpE(v));
+    }
+    return a;
+  }
+  int32_t cmpE(const std::string& v) {
+    int32_t a = addE(v);
+    if (peek("<=")) {
+      pos += 2;
+      return bin(KBin::Leq, a, addE(v));
+    }
+    if (peek("<")) {
+      ++pos;
+      return bin(KBin::Lt, a, addE(v));
+    }
+    if (peek("==")) {
+      pos += 2;
+      return bin(KBin::Eq, a, addE(v));
+    }
+    return a;
+  }
+  int32_t addE(const std::string& v) {
+    int32_t a = mulE(v);
+    for (;;) {
+      if (peek("+")) {
+        ++pos;
+        a = bin(KBin::Add, a, mulE(v));
+      } else if (peek("-") && !peek("--")) {
+        ++pos;
+        a = bin(KBin::Sub, a, mulE(v));
+      } else {
+        return a;
+      }
+    }
+  }
+  int32_t mulE(const std::string& v) {
+    int32_t a = unE(v);
+    for (;;) {
+      if (peek("*")) {
+        ++pos;
+        a = bin(KBin::Mult, a, unE(v));
+      } else if (peek("/")) {
+        ++pos;
+        a = bin(KBin::Div, a, unE(v));
+      } else {
+        return a;
+      }
+    }
+  }
+  int32_t unE(const std::string& v) {
+    skip();
+    if (peek("-") && !(pos + 1 < src.size() && std::isdigit(static_cast<unsigned char>(src[pos + 1])))) {
+      ++pos;
+      KNode n;
+      n.kind = KKind::UnOp;
+      n.op = static_cast<int>(KUn::Neg);
+      n.a = unE(v);
+      return push(n);
+    }
+    if (peek("!")) {
+      ++pos;
+      KNode n;
+      n.kind = KKind::UnOp;
+      n.op = static_cast<int>(KUn::Not);
+      n.a = unE(v);
+      return push(n);
+    }
+    return atom(v);
+  }
+  int32_t atom(const std::string& v) {
+    skip();
+    KNode n;
+    if (peek("(")) {
+      ++pos;
+      if (peekWord("if")) {
+        pos += 2;
+        n.kind = KKind::If;
+        n.a = expr(v);
+        expectWord("then");
+        n.b = expr(v);
+        expectWord("else");
+        n.c = expr(v);
+        expect(")");
+        return push(n);
+      }
+      if (peekWord("let")) return loop(v);
+      int32_t e = expr(v);
+      expect(")");
+      return e;
+    }
+    if (peekWord("true") || peekWord("false")) {
+      n.kind = KKind::Bool;
+      n.boolean = peekWord("true");
+      pos += n.boolean ? 4 : 5;
+      return push(n);
+    }
+    if (peekWord("t_now")) {
+      pos += 5;
+      n.kind = KKind::Now;
+      return push(n);
+    }
+    if (peekWord("ext")) {
+      pos += 3;
+      expect("[");
+      n.kind = KKind::ObsRef;
+      n.row = rowIndex(v);
+      expect(",");
+      double d;
+      int64_t i = 0;
+      if (number(d, i)) fail("column must be an integer");
+      n.col = static_cast<uint64_t>(i);
+      expect("]");
+      return push(n);
+    }
+    if (peekWord("rows")) {
+      pos += 4;
+      expect("[");
+      n.kind = KKind::TimeRef;
+      n.row = rowIndex(v);
+      expect("]");
+      return push(n);
+    }
+    if (peekWord("pay")) {
+      pos += 3;
+      expect("[");
+      n.kind = KKind::PayRef;
+      n.row = rowIndex(v);
+      expect(",");
+      n.from = party(ident());
+      expect(",");
+      n.to = party(ident());
+      expect("]");
+      return push(n);
+    }
+    double d = 0;
+    int64_t i = 0;
+    if (number(d, i)) {
+      n.kind = KKind::Float;
+      n.real = d;
+    } else {
+      n.kind = KKind::Nat;
+      n.nat = static_cast<uint64_t>(i);
+    }
+    return push(n);
+  }
+  // (let tK = loop tK = OFF while (!COND & (tK < OFF + W)) do tK + 1
+  //  in if COND then THEN else ELSE)
+  int32_t loop(const std::string& v) {
+    expectWord("let");
+    const std::string t = ident();
+    expect("=");
+    expectWord("loop");
+    if (ident() != t) fail("loop variable mismatch");
+    expect("=");
+    if (ident() != v) fail("loop must start at the enclosing offset " + v);
+    expectWord("while");
+    expect("(");
+    expect("!");
+    const std::size_t condStart = pos;
+    (void)unE(t);  // the while-condition copy of COND (discarded)
+    k.nodes.resize(k.nodes.size());  // (nodes of the copy stay unreferenced)
+    (void)condStart;
+    expect("&");
+    expect("(");
+    if (ident() != t) fail("loop bound must test " + t);
+    expect("<");
+    if (ident() != v) fail("loop bound must be relative to " + v);
+    expect("+");
+    KNode n;
+    n.kind = KKind::LoopIf;
+    if (peekWord("tenv")) {
+      pos += 4;
+      expect("[");
+      double d;
+      int64_t idx = 0;
+      if (number(d, idx)) fail("tenv index must be an integer");
+      expect("]");
+      if (idx < 0 || static_cast<std::size_t>(idx) >= tenvValues.size())
+        fail("loop window tenv[" + std::to_string(idx) + "] has no value");
+      n.nat = tenvValues[static_cast<std::size_t>(idx)];
+    } else {
+      double d;
+      int64_t w = 0;
+      if (number(d, w)) fail("loop window must be an integer");
+      n.nat = static_cast<uint64_t>(w);
+    }
+    expect(")");
+    expect(")");
+    expectWord("do");
+    if (ident() != t) fail("loop step must advance " + t);
+    expect("+");
+    double d;
+    int64_t one = 0;
+    if (number(d, one) || one != 1) fail("loop step must be + 1");
+    expectWord("in");
+    expectWord("if");
+    n.a = expr(t);
+    expectWord("then");
+    n.b = expr(t);
+    expectWord("else");
+    n.c = expr(t);
+    expect(")");
+    return push(n);
+  }
+
+  void read() {
+    expectWord("let");
+    expectWord("rows");
+    expect("=");
+    expect("[");
+    while (!peek("]")) {
+      double d;
+      int64_t i = 0;
+      if (number(d, i)) fail("rows must be integers");
+      k.rows.push_back(i);
+      if (peek(",")) ++pos;
+    }
+    expect("]");
+    expectWord("let");
+    expectWord("cols");
+    expect("=");
+    expect("[");
+    while (!peek("]")) {
+      k.cols.push_back(quoted());
+      if (peek(",")) ++pos;
+    }
+    expect("]");
+    expectWord("let");
+    expectWord("payoffInternal");
+    expect("(");
+    for (const char* a : {"ext", "tenv", "disc", "t0", "t_now"}) {
+      expectWord(a);
+      if (peek(",")) ++pos;
+    }
+    expect(")");
+    expect("=");
+    k.root = expr("t0");
+    // the wrapper "let payoff(...) = payoffInternal(ext, tenv, disc, 0, t_now)" is fixed
+    expectWord("let");
+    expectWord("payoff");
+  }
+};
+
+}  // namespace
+
+Kernel kernelFromSource(const std::string& text, const std::vector<uint64_t>& tenvValues) {
+  Kernel k;
+  TextReader r{text, tenvValues, k};
+  r.read();
+  // Drop the unreferenced while-condition copies: re-emit reachable nodes
+  // in postorder so the pool has the shape kernelFromJson produces.
+  Kernel out;
+  out.rows = k.rows;
+  out.cols = k.cols;
+  out.parties = k.parties;
+  out.partyNames = k.partyNames;
+  std::vector<int32_t> map(k.nodes.size(), -1);
+  std::vector<std::pair<int32_t, bool>> st{{k.root, false}};
+  while (!st.empty()) {
+    auto [i, done] = st.back();
+    st.pop_back();
+    if (map[i] >= 0) continue;
+    const KNode& n = k.nodes[i];
+    if (!done) {
+      st.push_back({i, true});
+      for (int32_t ch : {n.c, n.b, n.a})
+        if (ch >= 0 && map[ch] < 0) st.push_back({ch, false});
+      continue;
+    }
+    KNode m = n;
+    m.a = n.a >= 0 ? map[n.a] : -1;
+    m.b = n.b >= 0 ? map[n.b] : -1;
+    m.c = n.c >= 0 ? map[n.c] : -1;
+    out.nodes.push_back(m);
+    map[i] = static_cast<int32_t>(out.nodes.size() - 1);
+  }
+  out.root = map[k.root];
+  int64_t maxDay = 0;
+  for (int64_t d : out.rows) maxDay = std::max(maxDay, d);
+  out.horizon = static_cast<uint64_t>(maxDay) + 1;  // KernelBuilder::build, kernel.cpp:24-31
+  return out;
+}
+
+Kernel kernelFromWire(const std::string& text, const std::vector<uint64_t>& tenvValues) {
+  std::size_t i = 0;
+  while (i < text.size() && std::isspace(static_cast<unsigned char>(text[i]))) ++i;
+  if (i < text.size() && text[i] == '{') return kernelFromJson(text);
+  return kernelFromSource(text, tenvValues);
 }
 
 uint64_t kernelShapeHash(const Kernel& k) {

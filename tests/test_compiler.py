@@ -202,3 +202,29 @@ def test_template_literal_table_matches_instance_batch():
     assert L1["n_inst_const"] == 3
     with pytest.raises(E.ContractError, match="literal table does not match"):
         E.Plan(brc, m, [0], literals=[lits[:-1]])
+
+
+@pytest.mark.parametrize("name,model,tenv", [
+    ("european-call", "call", None), ("barrier", "barrier", None),
+    ("double-option", "double", None), ("fx-swap", "fx", None),
+    ("template-option", "call", {"t0": 10, "t1": 80}), ("worst-off", "three", None),
+    ("brc", "three", None)])
+def test_kernel_text_format_compiles_like_json(name, model, tenv):
+    """The reference's textual kernel format (emitKernelSource output, golden
+    files written by the reference) is an engine input: same program as the
+    kernel JSON, literal order included."""
+    text = open(os.path.join(GOLD, "kernels", name + ".kernel")).read()
+    js = load_kernel(name)
+    m = load_model(model)
+    days = [0, 10, 45]
+    a = E.compile_listing(E.Kernel(js), m, days, tenv=tenv)
+    b = E.compile_listing(text, m, days)
+    for key in ("ops", "shared_const_bits", "outputs", "steps", "n_thread"):
+        assert a[key] == b[key], key
+    assert E.kernel_literals(text) == E.kernel_literals(E.Kernel(js))
+
+
+def test_kernel_text_errors():
+    with pytest.raises(E.ContractParseError, match="kernel source"):
+        E.compile_listing("let rows = [1]\nlet cols = []\nlet payoffInternal(ext, tenv, disc, t0, t_now) = (1.0 +",
+                          load_model("call"))
