@@ -167,7 +167,9 @@ int cltk_debug_paths(cltk_plan* plan, uint64_t seed, uint64_t path0, uint64_t np
 int cltk_debug_rng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
                    uint64_t* bits, double* uniforms, double* normals, cltk_error* err);
 /* Device exp / log / erfc / invNormalCdf (fn = 0..3) of x[n] (host buffers):
- * the engine's bit-exact restatements of glibc's routines. */
+ * the engine's bit-exact restatements of glibc's routines; fn = 4: the
+ * engine's bounded-range division of the pairs (x[2i], x[2i+1]) (n even, the
+ * quotient written to both slots); fn = 5: its -x / sqrt(2.0). */
 int cltk_debug_math(int device, int fn, const double* x, uint64_t n, double* out,
                     cltk_error* err);
 /* Measured DFMA throughput (TFLOP/s) over `iters` iterations. */

@@ -449,9 +449,12 @@ def debug_rng(seed: int, path: int, i0: int, n: int, device: int = -1):
 
 def debug_math(fn: str, x, device: int = -1):
     """Device build of the engine's glibc-exact ``exp`` / ``log`` / ``erfc`` or
-    the reference's ``inv_normal`` (invNormalCdf) over an array."""
+    the reference's ``inv_normal`` (invNormalCdf) over an array; ``div``
+    (pairs ``x[2i] / x[2i+1]`` through the engine's bounded-range division,
+    written to both slots) and ``halley_arg`` (``-x / sqrt(2.0)``) check the
+    engine's division shortcuts against IEEE."""
     import numpy as np
-    code = {"exp": 0, "log": 1, "erfc": 2, "inv_normal": 3}[fn]
+    code = {"exp": 0, "log": 1, "erfc": 2, "inv_normal": 3, "div": 4, "halley_arg": 5}[fn]
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.zeros_like(x)
     err = _native.ErrorC()

@@ -88,9 +88,10 @@ __constant__ double kAck[32] = {
     7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
     3.754408661907416e+00,
     // 21: plow, 22: 1 - plow (as the reference folds it), 23: sqrt(2.0),
-    // 24: sqrt(2.0 * M_PI), 25: 0.5, 26: -0.5, 27: 1.0, 28: -2.0, 29: 2^-53
+    // 24: sqrt(2.0 * M_PI), 25: 0.5, 26: -0.5, 27: 1.0, 28: -2.0, 29: 2^-53,
+    // 30: RN(1 / sqrt(2.0))
     0.02425, 0x1.f395810624dd3p-1, 0x1.6a09e667f3bcdp+0, 0x1.40d931ff62705p+1,
-    0.5, -0.5, 1.0, -2.0, 0x1.0p-53, 0.0, 0.0};
+    0.5, -0.5, 1.0, -2.0, 0x1.0p-53, 0x1.6a09e667f3bccp-1, 0.0};
 
 __device__ __forceinline__ bool acklam_is_central(double p) {
   return p >= kAck[21] && p <= kAck[22];
@@ -103,7 +104,7 @@ __device__ __forceinline__ double acklam_central(double p) {
   const double r = M_(q, q);
   const double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[0], r), K[1]), r), K[2]), r), K[3]), r), K[4]), r), K[5]);
   const double den = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[6], r), K[7]), r), K[8]), r), K[9]), r), K[10]), r), K[27]);
-  return __ddiv_rn(M_(num, q), den);
+  return cltk_gm::div_inrange(M_(num, q), den);  // |num q| >= 2^-56, den in (0.2, 1]
 }
 
 // Tail rational (p < plow or p > 1 - plow).
@@ -113,11 +114,19 @@ __device__ __forceinline__ double acklam_tail(double p) {
   const double q = __dsqrt_rn(M_(K[28], cltk_gm::log(lower ? p : A_(K[27], -p))));
   const double num = A_(M_(A_(M_(A_(M_(A_(M_(A_(M_(K[11], q), K[12]), q), K[13]), q), K[14]), q), K[15]), q), K[16]);
   const double den = A_(M_(A_(M_(A_(M_(A_(M_(K[17], q), K[18]), q), K[19]), q), K[20]), q), K[27]);
-  return __ddiv_rn(lower ? num : -num, den);
+  return cltk_gm::div_inrange(lower ? num : -num, den);
 }
 
-// erfc argument of the Halley step: -x / sqrt(2.0)
-__device__ __forceinline__ double halley_arg(double x) { return __ddiv_rn(-x, kAck[23]); }
+// erfc argument of the Halley step: -x / sqrt(2.0), correctly rounded by
+// Markstein's division by a constant (y = RN(1/c); q = RN(a y) is within an
+// ulp of a/c, the residual a - q c is exact, and RN(q + r y) = RN(a/c) for
+// normal-range a): three FP64 operations instead of a full division.
+__device__ __forceinline__ double halley_arg(double x) {
+  const double a = -x;
+  const double q = __dmul_rn(a, kAck[30]);
+  const double r = __fma_rn(-q, kAck[23], a);
+  return __fma_rn(r, kAck[30], q);
+}
 
 // Halley step given ef = erfc(-x/sqrt(2)):
 //   e = 0.5*ef - p; u = e*sqrt(2*pi)*exp(x*x/2); x - u/(1 + x*u/2)
@@ -125,7 +134,8 @@ __device__ __forceinline__ double halley(double x, double p, double ef) {
   const double* K = kAck;
   const double e = A_(M_(K[25], ef), -p);
   const double u = M_(M_(e, K[24]), cltk_gm::exp(M_(M_(x, x), K[25])));
-  return A_(x, -__ddiv_rn(u, A_(K[27], M_(M_(x, u), K[25]))));
+  // u = +0 or |u| >= 2^-110; the divisor is 1 + O(u)
+  return A_(x, -cltk_gm::div_inrange(u, A_(K[27], M_(M_(x, u), K[25]))));
 }
 
 // invNormalCdf for one value (reference and test paths).
@@ -171,13 +181,15 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 #define CLTK_MIN_BLOCKS 6
 #endif
 constexpr int kMaxBatch = CLTK_MAX_BATCH;
-// doubles: X, P, Y slots + the per-warp work lists (3 * 32 * kMaxBatch u16)
-constexpr size_t kNormScratchWords = 3 * kMaxBatch * kBlock + (kWarps * 3 * 32 * kMaxBatch + 3) / 4;
+// doubles: X, P, Y slots + the per-warp work lists (3 * 32 * kMaxBatch bytes)
+// list items are (slot << 5 | lane) bytes
+static_assert(kMaxBatch * 32 <= 256, "work-list items must fit a byte");
+constexpr size_t kNormScratchWords = 3 * kMaxBatch * kBlock + (kWarps * 3 * 32 * kMaxBatch + 7) / 8;
 struct NormScratch {
   double* X;
   double* P;
   double* Y;
-  uint16_t* list;  // this warp's 3 work lists of 32 * kMaxBatch (slot, lane) items
+  uint8_t* list;   // this warp's 3 work lists of 32 * kMaxBatch (slot, lane) items
 };
 __host__ __device__ constexpr int batchSteps(int na) { return na >= kMaxBatch ? 1 : kMaxBatch / na; }
 
@@ -272,14 +284,25 @@ __device__ __noinline__ void run_ops(const Frame f, const uint64_t* __restrict__
 // memory (ballot + popc prefix); the list is then dealt out 32 items at a
 // time, so a branch that only a few lanes of a few slots need costs
 // ceil(items / 32) passes instead of one pass per slot.
-__device__ __forceinline__ void list_push(uint16_t* list, int& count, bool pred, int m, int lane) {
+// The push is branch-free: every lane forms its slot address, the store is
+// predicated (no divergent region around it).
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ void list_push(uint8_t* list, int& count, bool pred, int m, int lane) {
   const uint32_t bal = __ballot_sync(0xffffffffu, pred);
-  if (pred) list[count + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint16_t>((m << 5) | lane);
+  const uint32_t addr = smem_addr(list) + static_cast<uint32_t>(count) + __popc(bal & lanemask_lt());
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u8 [%0], %1;\n\t}" ::"r"(addr),
+      "r"(static_cast<uint32_t>((m << 5) | lane)), "r"(static_cast<uint32_t>(pred))
+      : "memory");
   count += __popc(bal);
 }
 
 template <class F>
-__device__ __forceinline__ void list_each(const uint16_t* list, int count, int lane, F f) {
+__device__ __forceinline__ void list_each(const uint8_t* list, int count, int lane, F f) {
   __syncwarp();
   const int wbase = threadIdx.x & ~31;
   for (int base = 0; base < count; base += 32) {
@@ -300,9 +323,9 @@ __device__ __forceinline__ void list_each(const uint16_t* list, int count, int l
 __device__ __forceinline__ bool normals_batch(const PhiloxKeys& K, uint64_t path, uint64_t i0,
                                               int M, uint32_t drawMask, const NormScratch NS) {
   const int tid = threadIdx.x, lane = tid & 31;
-  uint16_t* tails = NS.list;
-  uint16_t* r2 = NS.list + 32 * kMaxBatch;
-  uint16_t* r3 = NS.list + 64 * kMaxBatch;
+  uint8_t* tails = NS.list;
+  uint8_t* r2 = NS.list + 32 * kMaxBatch;
+  uint8_t* r3 = NS.list + 64 * kMaxBatch;
   int nTail = 0, n2 = 0, n3 = 0;
   bool ok = true;
   // 1: uniforms; central rational for every lane; tails listed
@@ -457,7 +480,7 @@ __device__ __forceinline__ void qmc_normals_batch(const DevPlan& P, const uint32
                                                   uint64_t path, bool aligned, uint32_t c0,
                                                   int nC, const NormScratch NS) {
   const int tid = threadIdx.x, lane = tid & 31;
-  uint16_t* tails = NS.list;
+  uint8_t* tails = NS.list;
   int nTail = 0;
   const uint64_t gray = path ^ (path >> 1);
   const uint32_t G = static_cast<uint32_t>(gray >> 5), glow = static_cast<uint32_t>(gray & 31u);
@@ -662,7 +685,7 @@ __global__ void __launch_bounds__(kBlock, CLTK_MIN_BLOCKS) path_kernel(const Dev
                                   static_cast<size_t>(h.n_bridge_slots) * NA * kBlock)
                             : static_cast<size_t>(kMaxBatch) * kBlock;
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
-                 reinterpret_cast<uint16_t*>(nsBase + 2 * kMaxBatch * kBlock + yWords) +
+                 reinterpret_cast<uint8_t*>(nsBase + 2 * kMaxBatch * kBlock + yWords) +
                      warp * 3 * 32 * kMaxBatch};
   double* WS = nsBase + 2 * kMaxBatch * kBlock;
 
@@ -809,7 +832,7 @@ __global__ void __launch_bounds__(kBlock) dump_kernel(const DevPlan P, const Dum
                                   static_cast<size_t>(h.n_bridge_slots) * NA * kBlock)
                             : static_cast<size_t>(kMaxBatch) * kBlock;
   NormScratch NS{nsBase, nsBase + kMaxBatch * kBlock, nsBase + 2 * kMaxBatch * kBlock,
-                 reinterpret_cast<uint16_t*>(nsBase + 2 * kMaxBatch * kBlock + yWords) +
+                 reinterpret_cast<uint8_t*>(nsBase + 2 * kMaxBatch * kBlock + yWords) +
                      warp * 3 * 32 * kMaxBatch};
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kBlock + tid;
   const bool active = idx < D.npaths;
@@ -863,8 +886,12 @@ __global__ void math_kernel(int fn, const double* __restrict__ x, uint64_t n, do
   const uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const double v = x[k];
+  if (fn == 4) {  // pairs (a, b): the bounded-range division, a / b in both slots
+    out[k] = cltk_gm::div_inrange(x[k & ~1ull], x[k | 1ull]);
+    return;
+  }
   out[k] = fn == 0 ? cltk_gm::exp(v) : fn == 1 ? cltk_gm::log(v) : fn == 2 ? cltk_gm::erfc(v)
-                                                                 : inv_normal(v);
+         : fn == 5 ? halley_arg(v) : inv_normal(v);
 }
 
 // DFMA throughput probe: 8 independent chains per thread.
