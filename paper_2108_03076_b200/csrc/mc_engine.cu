@@ -178,7 +178,7 @@ __device__ __forceinline__ void sts64(uint32_t a, double v) {
 #define CLTK_ILP2 0
 #endif
 #ifndef CLTK_MIN_BLOCKS
-#define CLTK_MIN_BLOCKS 6
+#define CLTK_MIN_BLOCKS 7
 #endif
 constexpr int kMaxBatch = CLTK_MAX_BATCH;
 // doubles: X, P, Y slots + the per-warp work lists (3 * 32 * kMaxBatch bytes)
@@ -204,7 +204,7 @@ __device__ __forceinline__ int64_t bits_of(double v) { return __double_as_longlo
 __device__ __forceinline__ double of_bits(int64_t v) { return __longlong_as_double(v); }
 
 #define CLTK_VEC_LOOP(EXPR)                                                  \
-  for (uint32_t i = 0; i < n; ++i) {                                         \
+  _Pragma("unroll 1") for (uint32_t i = 0; i < n; ++i) {                     \
     const uint64_t u = __ldg(code + pc + i);                                 \
     const double va = ld(f, static_cast<uint32_t>(u >> 22) & 0x3fff);       \
     const double vb = ld(f, static_cast<uint32_t>(u >> 36) & 0x3fff);       \
