@@ -15,10 +15,13 @@ CXXFLAGS := -std=c++17 -O2 -fPIC -ffp-contract=off -Wall -Wno-unused-function \
 NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -ccbin $(HOSTCXX) \
             -Xcompiler -fPIC -Xptxas -v -Iinclude
 
-HOST_SRCS := host_model compiler engine capi sobol_table
-HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS)))
+HOST_SRCS := host_model compiler engine capi sobol_table jit
+HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS))) $(OBJ)/jit_sources.o
+# device headers embedded for the NVRTC build (csrc/jit.cpp)
+JIT_HDRS  := $(SRC)/engine_device.cuh $(SRC)/engine_types.h $(SRC)/program.h \
+             $(SRC)/glibc_math.h $(SRC)/glibc_tables.h
 CU_OBJS   := $(OBJ)/mc_engine.o
-HDRS      := $(wildcard $(SRC)/*.hpp $(SRC)/*.h) include/cltk_b200.h
+HDRS      := $(wildcard $(SRC)/*.hpp $(SRC)/*.h $(SRC)/*.cuh) include/cltk_b200.h
 
 .PHONY: all lib oracle testlib clean
 all: lib oracle testlib
@@ -29,13 +32,20 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJ)
 	$(HOSTCXX) $(CXXFLAGS) -c $< -o $@
 
-$(OBJ)/mc_engine.o: $(SRC)/mc_engine.cu $(HDRS)
+$(OBJ)/jit_sources.cpp: $(JIT_HDRS) tools/embed_sources.py
+	@mkdir -p $(OBJ)
+	python3 tools/embed_sources.py $@ $(JIT_HDRS)
+
+$(OBJ)/jit_sources.o: $(OBJ)/jit_sources.cpp
+	$(HOSTCXX) $(CXXFLAGS) -c $< -o $@
+
+$(OBJ)/mc_engine.o: $(SRC)/mc_engine.cu $(HDRS) $(SRC)/engine_device.cuh
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/mc_engine.ptxas.txt || (cat $(OBJ)/mc_engine.ptxas.txt; false)
 	@grep -E "Used|spill" $(OBJ)/mc_engine.ptxas.txt | head -40
 
 $(LIB): $(HOST_OBJS) $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -cudart static -o $@ $^
+	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -cudart static -o $@ $^ -ldl
 
 oracle:
 	$(MAKE) -C oracle all

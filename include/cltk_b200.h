@@ -56,6 +56,7 @@ typedef struct {
   uint32_t n_instances, n_days, n_outputs;
   uint32_t n_shared_ops, n_inst_ops, has_err, block;
   uint64_t kernel_nodes, dag_nodes;
+  uint32_t jit; /* 1: the plan runs its NVRTC-generated kernel */
 } cltk_plan_info;
 
 /* Chunk partial written by cltk_plan_launch: count, mean, sum of squared
@@ -67,12 +68,19 @@ typedef struct {
 /* Engine options.  rng: 0 = Philox2x64-10 + Acklam/Halley (the reference's
  * generator; bit-exact per path), 1 = Sobol (Joe-Kuo, 32-bit) + Wichura AS241
  * + Brownian bridge over the drawing days (QMC; seed != 0 applies a
- * per-dimension digital shift).  rewrite: exact OR/AND->min/max rewrite. */
+ * per-dimension digital shift).  rewrite: exact OR/AND->min/max rewrite.
+ * jit: payoff evaluation -- 0 = bytecode interpreter in the ahead-of-time
+ * kernel, 1 = the payoff program compiled to CUDA and built with NVRTC for
+ * sm_100a at plan creation (cached by program shape; literals stay kernel
+ * data, so new template instances do not recompile; error if NVRTC is
+ * unavailable), 2 = NVRTC when available and the program is small, else 0.
+ * Both give bit-identical results. */
 typedef struct {
   int device;   /* -1: current */
   int rewrite;  /* default 1 */
   int rng;      /* default 0 */
-  int reserved[5];
+  int jit;      /* default 0 */
+  int reserved[4];
 } cltk_options;
 
 const char* cltk_version(void);
@@ -90,6 +98,12 @@ int cltk_gpu_price_batch(const char* const* kernel_jsons, size_t n_instances,
                          const char* model_json, uint64_t paths, uint64_t seed,
                          const uint64_t* days, size_t n_days, const char* tenv_json, int device,
                          cltk_price_result* results, cltk_error* err);
+/* cltk_gpu_price_batch with engine options (rng mode, NVRTC payoff kernel). */
+int cltk_gpu_price_batch_ex(const char* const* kernel_jsons, size_t n_instances,
+                            const char* model_json, uint64_t paths, uint64_t seed,
+                            const uint64_t* days, size_t n_days, const char* tenv_json,
+                            const cltk_options* opts, cltk_price_result* results,
+                            cltk_error* err);
 
 /* Template batch as "template parameters passed as kernel arguments": one
  * kernel and literals[n_instances][n_literals], the values of its float
@@ -126,6 +140,11 @@ int cltk_plan_create_template(const char* kernel_json, const double* literals, s
 int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const char* model_json,
                      const uint64_t* days, size_t n_days, const char* tenv_json, int device,
                      int rewrite, cltk_plan** plan, cltk_error* err);
+/* cltk_plan_create with engine options (rng mode, NVRTC payoff kernel). */
+int cltk_plan_create_batch_ex(const char* const* kernel_jsons, size_t n_instances,
+                              const char* model_json, const uint64_t* days, size_t n_days,
+                              const char* tenv_json, const cltk_options* opts, cltk_plan** plan,
+                              cltk_error* err);
 void cltk_plan_destroy(cltk_plan* plan);
 int cltk_plan_get_info(const cltk_plan* plan, cltk_plan_info* info);
 /* Deterministic chunking of [0, paths): depends only on paths and the
@@ -153,6 +172,15 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
                          const char* model_json, const uint64_t* days, size_t n_days,
                          const char* tenv_json, int rewrite, int rng, char** json,
                          cltk_error* err);
+/* Host-only: the CUDA source the NVRTC mode generates for this program
+ * (malloc'd; free with cltk_free).  Replaces no reference interface (the
+ * reference interprets its kernel tree, proj/src/kernel.cpp:229-310). */
+int cltk_jit_source(const char* kernel_json, const char* model_json, const uint64_t* days,
+                    size_t n_days, const char* tenv_json, int rewrite, int rng, char** source,
+                    cltk_error* err);
+/* Host-only: NVRTC-compile a generated source for sm_100a (no device needed);
+ * cubin size and the compiler log (malloc'd). */
+int cltk_jit_compile(const char* source, uint64_t* cubin_bytes, char** log, cltk_error* err);
 /* Program listing (JSON, malloc'd; free with cltk_free). */
 int cltk_plan_dump(const cltk_plan* plan, char** json);
 void cltk_free(void* p);

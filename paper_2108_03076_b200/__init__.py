@@ -36,7 +36,7 @@ __all__ = [
     "Kernel", "ContractError", "ContractParseError", "ContractTypeError",
     "ContractUnsupportedError", "price", "price_batch", "black_scholes_call", "Plan",
     "compile_listing", "debug_rng", "debug_math", "fp64_peak", "load_kernel", "version",
-    "kernel_literals", "price_template",
+    "kernel_literals", "price_template", "jit_source", "jit_compile",
 ]
 
 
@@ -203,13 +203,19 @@ def _results(arr, n: int) -> list[dict]:
 
 
 RNG_MODES = {"philox": 0, "sobol": 1}
+# payoff evaluation: bytecode interpreter / NVRTC-generated kernel / NVRTC when
+# available and the program is small (results are bit-identical)
+JIT_MODES = {False: 0, True: 1, "auto": 2}
 
 
-def _options(device: int = -1, rewrite: bool = True, rng: str = "philox"):
+def _options(device: int = -1, rewrite: bool = True, rng: str = "philox", jit=False):
     if rng not in RNG_MODES:
         raise ValueError(f"rng must be one of {sorted(RNG_MODES)}")
+    if jit not in JIT_MODES:
+        raise ValueError("jit must be False, True or 'auto'")
     o = _native.OptionsC()
     o.device, o.rewrite, o.rng = int(device), int(bool(rewrite)), RNG_MODES[rng]
+    o.jit = JIT_MODES[jit]
     return o
 
 
@@ -219,23 +225,25 @@ def version() -> str:
 
 def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, seed: int = 0,
           days: Sequence[int] = (0,), tenv: dict | None = None, threads: int = 0,
-          device: int = -1, rng: str = "philox") -> list[dict]:
+          device: int = -1, rng: str = "philox", jit=False) -> list[dict]:
     """priceAcrossTime on the GPU (cltk.price, proj/python/bindings.cpp:103-126).
 
     Returns one dict per valuation day: ``price``, ``std_error``, ``paths``,
     ``seed``, ``valuation_day``.  ``threads`` is accepted for compatibility
     (results never depend on it).  ``rng="philox"`` (default) reproduces the
     reference's per-path values bit for bit; ``rng="sobol"`` is the QMC mode
-    (Sobol + AS241 + Brownian bridge)."""
+    (Sobol + AS241 + Brownian bridge).  ``jit=True`` evaluates the payoff
+    with the NVRTC-generated kernel instead of the bytecode interpreter
+    (bit-identical results)."""
     L = _native.lib()
     d, nd = _days(days)
     out = (_native.PriceResultC * max(1, nd))()
     err = _native.ErrorC()
-    if rng == "philox":
+    if rng == "philox" and not jit:
         rc = L.cltk_gpu_price(_kernel_json(kernel), _model_json(model), int(paths), int(seed), d,
                               nd, _tenv_json(tenv), int(threads), int(device), out, C.byref(err))
     else:
-        o = _options(device, True, rng)
+        o = _options(device, True, rng, jit)
         rc = L.cltk_gpu_price_ex(_kernel_json(kernel), None, 1, 0, _model_json(model), int(paths),
                                  int(seed), d, nd, _tenv_json(tenv), C.byref(o), out,
                                  C.byref(err))
@@ -245,7 +253,7 @@ def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, s
 
 def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths: int = 100000,
                 seed: int = 0, days: Sequence[int] = (0,), tenv: dict | None = None,
-                device: int = -1) -> list[list[dict]]:
+                device: int = -1, rng: str = "philox", jit=False) -> list[list[dict]]:
     """Price literal instances of one template on one shared path set (no
     recompilation per instance): ``[instance][day]`` result dicts."""
     L = _native.lib()
@@ -254,8 +262,13 @@ def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths
     arr = (C.c_char_p * n)(*[_kernel_json(k) for k in kernels])
     out = (_native.PriceResultC * max(1, n * nd))()
     err = _native.ErrorC()
-    rc = L.cltk_gpu_price_batch(arr, n, _model_json(model), int(paths), int(seed), d, nd,
-                                _tenv_json(tenv), int(device), out, C.byref(err))
+    if rng == "philox" and not jit:
+        rc = L.cltk_gpu_price_batch(arr, n, _model_json(model), int(paths), int(seed), d, nd,
+                                    _tenv_json(tenv), int(device), out, C.byref(err))
+    else:
+        o = _options(device, True, rng, jit)
+        rc = L.cltk_gpu_price_batch_ex(arr, n, _model_json(model), int(paths), int(seed), d, nd,
+                                       _tenv_json(tenv), C.byref(o), out, C.byref(err))
     _raise(rc, err)
     flat = _results(out, n * nd)
     return [flat[i * nd:(i + 1) * nd] for i in range(n)]
@@ -277,7 +290,7 @@ def kernel_literals(kernel: Kernel | str | dict) -> list[float]:
 def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
                    paths: int = 100000, seed: int = 0, days: Sequence[int] = (0,),
                    tenv: dict | None = None, device: int = -1,
-                   rng: str = "philox") -> list[list[dict]]:
+                   rng: str = "philox", jit=False) -> list[list[dict]]:
     """Price instances of one template given as a literal table
     ``literals[instance][j]`` (j in ``kernel_literals`` order): one compile,
     one path set, the literals passed to the kernel as data."""
@@ -290,7 +303,7 @@ def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
     n = lit.shape[0]
     out = (_native.PriceResultC * max(1, n * nd))()
     err = _native.ErrorC()
-    o = _options(device, True, rng)
+    o = _options(device, True, rng, jit)
     rc = L.cltk_gpu_price_ex(_kernel_json(kernel), lit.ctypes.data, n, lit.shape[1],
                              _model_json(model), int(paths), int(seed), d, nd, _tenv_json(tenv),
                              C.byref(o), out, C.byref(err))
@@ -323,13 +336,42 @@ def compile_listing(kernels: Sequence[Kernel | str | dict] | Kernel, model: str 
     return _deep(json.loads, s)
 
 
+def jit_source(kernel: Kernel | str | dict, model: str | dict, days: Sequence[int] = (0,),
+               tenv: dict | None = None, rewrite: bool = True, rng: str = "philox") -> str:
+    """Host-only: the CUDA source of the NVRTC payoff kernel for this program."""
+    L = _native.lib()
+    d, nd = _days(days)
+    out = C.c_void_p()
+    err = _native.ErrorC()
+    rc = L.cltk_jit_source(_kernel_json(kernel), _model_json(model), d, nd, _tenv_json(tenv),
+                           int(rewrite), RNG_MODES[rng], C.byref(out), C.byref(err))
+    _raise(rc, err)
+    s = C.cast(out, C.c_char_p).value.decode()
+    L.cltk_free(out)
+    return s
+
+
+def jit_compile(source: str) -> tuple[int, str]:
+    """Host-only NVRTC compile of a generated source for sm_100a:
+    (cubin bytes, compiler log).  Raises UnsupportedError on failure."""
+    L = _native.lib()
+    n = C.c_uint64()
+    out = C.c_void_p()
+    err = _native.ErrorC()
+    rc = L.cltk_jit_compile(source.encode(), C.byref(n), C.byref(out), C.byref(err))
+    _raise(rc, err)
+    log = C.cast(out, C.c_char_p).value.decode()
+    L.cltk_free(out)
+    return n.value, log
+
+
 class Plan:
     """Compiled plan on one device: the building block of multi-GPU pricing
     (see ``paper_2108_03076_b200.distributed``)."""
 
     def __init__(self, kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
                  days: Sequence[int] = (0,), tenv: dict | None = None, device: int = -1,
-                 rewrite: bool = True, literals=None, rng: str = "philox"):
+                 rewrite: bool = True, literals=None, rng: str = "philox", jit=False):
         if not isinstance(kernels, (list, tuple)):
             kernels = [kernels]
         self._L = _native.lib()
@@ -337,24 +379,22 @@ class Plan:
         d, nd = _days(self.days)
         self._h = C.c_void_p()
         err = _native.ErrorC()
-        if literals is not None or rng != "philox":
+        if literals is not None:
             import numpy as np
-            o = _options(device, rewrite, rng)
-            if literals is not None:
-                lit = np.ascontiguousarray(literals, dtype=np.float64)
-                lp, n_i, n_l = lit.ctypes.data, lit.shape[0], lit.shape[1]
-            else:
-                lit, lp, n_i, n_l = None, None, 1, 0
+            o = _options(device, rewrite, rng, jit)
+            lit = np.ascontiguousarray(literals, dtype=np.float64)
+            lp, n_i, n_l = lit.ctypes.data, lit.shape[0], lit.shape[1]
             if len(kernels) != 1:
-                raise ValueError("rng/literals plans take one template kernel")
+                raise ValueError("literal-table plans take one template kernel")
             rc = self._L.cltk_plan_create_ex(
                 _kernel_json(kernels[0]), lp, n_i, n_l, _model_json(model), d, nd,
                 _tenv_json(tenv), C.byref(o), C.byref(self._h), C.byref(err))
         else:
             arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
-            rc = self._L.cltk_plan_create(arr, len(kernels), _model_json(model), d, nd,
-                                          _tenv_json(tenv), int(device), int(rewrite),
-                                          C.byref(self._h), C.byref(err))
+            o = _options(device, rewrite, rng, jit)
+            rc = self._L.cltk_plan_create_batch_ex(arr, len(kernels), _model_json(model), d, nd,
+                                                   _tenv_json(tenv), C.byref(o),
+                                                   C.byref(self._h), C.byref(err))
         _raise(rc, err)
         info = _native.PlanInfoC()
         self._L.cltk_plan_get_info(self._h, C.byref(info))

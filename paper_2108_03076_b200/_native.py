@@ -20,13 +20,14 @@ EXPORTS = [
     "cltk_compile_listing", "cltk_plan_dump", "cltk_free", "cltk_debug_paths", "cltk_debug_rng", "cltk_debug_math",
     "cltk_fp64_peak", "cltk_black_scholes_call", "cltk_gpu_price_template",
     "cltk_kernel_literals", "cltk_plan_create_template", "cltk_gpu_price_ex",
-    "cltk_plan_create_ex",
+    "cltk_plan_create_ex", "cltk_jit_source", "cltk_jit_compile",
+    "cltk_plan_create_batch_ex", "cltk_gpu_price_batch_ex",
 ]
 
 
 class OptionsC(C.Structure):
-    _fields_ = [("device", C.c_int), ("rewrite", C.c_int), ("rng", C.c_int),
-                ("reserved", C.c_int * 5)]
+    _fields_ = [("device", C.c_int), ("rewrite", C.c_int), ("rng", C.c_int), ("jit", C.c_int),
+                ("reserved", C.c_int * 4)]
 
 
 class PriceResultC(C.Structure):
@@ -42,7 +43,7 @@ class PlanInfoC(C.Structure):
     _fields_ = [(n, C.c_uint32) for n in (
         "n_assets", "n_steps", "n_thread", "n_shared_const", "n_inst_const", "n_instances",
         "n_days", "n_outputs", "n_shared_ops", "n_inst_ops", "has_err", "block")] + [
-        ("kernel_nodes", C.c_uint64), ("dag_nodes", C.c_uint64)]
+        ("kernel_nodes", C.c_uint64), ("dag_nodes", C.c_uint64), ("jit", C.c_uint32)]
 
 
 _lib = None
@@ -102,6 +103,16 @@ def lib() -> C.CDLL:
     L.cltk_plan_create_ex.restype = i32
     L.cltk_plan_create_ex.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t, cp, PO,
                                       C.POINTER(vp), PE]
+    L.cltk_jit_source.restype = i32
+    L.cltk_jit_source.argtypes = [cp, cp, P64, C.c_size_t, cp, i32, i32, C.POINTER(vp), PE]
+    L.cltk_jit_compile.restype = i32
+    L.cltk_jit_compile.argtypes = [cp, P64, C.POINTER(vp), PE]
+    L.cltk_plan_create_batch_ex.restype = i32
+    L.cltk_plan_create_batch_ex.argtypes = [C.POINTER(cp), C.c_size_t, cp, P64, C.c_size_t, cp, PO,
+                                            C.POINTER(vp), PE]
+    L.cltk_gpu_price_batch_ex.restype = i32
+    L.cltk_gpu_price_batch_ex.argtypes = [C.POINTER(cp), C.c_size_t, cp, u64, u64, P64,
+                                          C.c_size_t, cp, PO, PR, PE]
     L.cltk_plan_dump.restype = i32
     L.cltk_plan_dump.argtypes = [vp, C.POINTER(vp)]
     L.cltk_free.argtypes = [vp]

@@ -9,6 +9,7 @@
 #include "../../include/cltk_b200.h"
 #include "cltk_b200.hpp"
 #include "compiler.hpp"
+#include "jit.hpp"
 #include "engine_launch.hpp"
 
 using namespace cltk::b200;
@@ -155,6 +156,7 @@ RunOptions optionsOf(const cltk_options* o) {
     r.device = o->device;
     r.rewrite = o->rewrite != 0;
     r.rng = o->rng;
+    r.jit = o->jit;
   }
   return r;
 }
@@ -222,6 +224,42 @@ int cltk_plan_create(const char* const* kernel_jsons, size_t n_instances, const 
     opt.rewrite = rewrite != 0;
     p->plan = std::make_unique<Plan>(ptrs, m, d, tenvOf(tenv_json), opt);
     *out = p.release();
+  });
+}
+
+int cltk_plan_create_batch_ex(const char* const* kernel_jsons, size_t n_instances,
+                              const char* model_json, const uint64_t* days, size_t n_days,
+                              const char* tenv_json, const cltk_options* opts, cltk_plan** out,
+                              cltk_error* err) {
+  return guarded(err, [&] {
+    auto p = std::make_unique<cltk_plan>();
+    std::vector<const Kernel*> ptrs;
+    for (size_t i = 0; i < n_instances; ++i) {
+      p->kernels.push_back(std::make_unique<Kernel>(kernelFromWire(kernel_jsons[i])));
+      ptrs.push_back(p->kernels.back().get());
+    }
+    ModelSpec m = modelFromJson(model_json);
+    p->plan = std::make_unique<Plan>(ptrs, m, std::vector<uint64_t>(days, days + n_days),
+                                     tenvOf(tenv_json), optionsOf(opts));
+    *out = p.release();
+  });
+}
+
+int cltk_gpu_price_batch_ex(const char* const* kernel_jsons, size_t n_instances,
+                            const char* model_json, uint64_t paths, uint64_t seed,
+                            const uint64_t* days, size_t n_days, const char* tenv_json,
+                            const cltk_options* opts, cltk_price_result* results,
+                            cltk_error* err) {
+  return guarded(err, [&] {
+    std::vector<Kernel> ks;
+    ks.reserve(n_instances);
+    for (size_t i = 0; i < n_instances; ++i) ks.push_back(kernelFromWire(kernel_jsons[i]));
+    std::vector<const Kernel*> ptrs;
+    for (auto& k : ks) ptrs.push_back(&k);
+    ModelSpec m = modelFromJson(model_json);
+    toC(priceBatch(ptrs, m, paths, seed, std::vector<uint64_t>(days, days + n_days),
+                   tenvOf(tenv_json), optionsOf(opts)),
+        results);
   });
 }
 
@@ -310,6 +348,36 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
     char* p = static_cast<char*>(std::malloc(P.listing.size() + 1));
     std::memcpy(p, P.listing.c_str(), P.listing.size() + 1);
     *json = p;
+  });
+}
+
+int cltk_jit_source(const char* kernel_json, const char* model_json, const uint64_t* days,
+                    size_t n_days, const char* tenv_json, int rewrite, int rng, char** source,
+                    cltk_error* err) {
+  return guarded(err, [&] {
+    Kernel k = kernelFromWire(kernel_json);
+    ModelSpec m = modelFromJson(model_json);
+    SimPlanHost sp = buildSimPlan(k, m, static_cast<uint32_t>(rng));
+    TEnv t = tenvOf(tenv_json);
+    for (const auto& v : k.tvars) (void)t.lookup(v);
+    CompileOptions co;
+    co.rewrite = rewrite != 0;
+    std::vector<const Kernel*> ptrs{&k};
+    CompiledProgram P = compileProgram(ptrs, sp, std::vector<uint64_t>(days, days + n_days), co);
+    const std::string src = jitSource(P);
+    char* p = static_cast<char*>(std::malloc(src.size() + 1));
+    std::memcpy(p, src.c_str(), src.size() + 1);
+    *source = p;
+  });
+}
+
+int cltk_jit_compile(const char* source, uint64_t* cubin_bytes, char** log, cltk_error* err) {
+  return guarded(err, [&] {
+    std::string lg;
+    *cubin_bytes = jitCompileOnly(source, &lg);
+    char* p = static_cast<char*>(std::malloc(lg.size() + 1));
+    std::memcpy(p, lg.c_str(), lg.size() + 1);
+    *log = p;
   });
 }
 

@@ -143,6 +143,10 @@ struct RunOptions {
   // 1: Sobol (Joe-Kuo, 32-bit) + Wichura AS241 + Brownian bridge (QMC;
   //    seed != 0 applies a Philox-derived digital shift per dimension).
   int rng = 0;
+  // Payoff evaluation: 0 = bytecode interpreter (ahead-of-time kernel),
+  // 1 = NVRTC-generated kernel (jit.cpp; error if NVRTC is unavailable),
+  // 2 = NVRTC when available and the program is small enough, else 0.
+  int jit = 0;
 };
 
 // ---- compiled plan (host + device state) ------------------------------------
@@ -152,6 +156,7 @@ struct PlanInfo {
   uint32_t n_instances, n_days, n_outputs;
   uint32_t n_shared_ops, n_inst_ops, has_err, block;
   uint64_t kernel_nodes, dag_nodes;
+  uint32_t jit;  // 1: the plan runs the NVRTC-generated kernel
 };
 
 class Plan {

@@ -13,6 +13,7 @@
 #include "cltk_b200.hpp"
 #include "compiler.hpp"
 #include "engine_launch.hpp"
+#include "jit.hpp"
 
 namespace cltk {
 namespace b200 {
@@ -46,6 +47,7 @@ uint64_t philoxHost(uint64_t key, uint64_t c0, uint64_t c1) {
   return c0 ^ c1;
 }
 constexpr uint64_t kPartialBudget = 1ULL << 30;  // bytes of chunk partials
+constexpr size_t kJitAutoMaxOps = 4096;          // JIT_AUTO: larger programs stay interpreted
 
 }  // namespace
 
@@ -71,6 +73,7 @@ struct PlanImpl {
   bool accInSmem = true;
   int blocksPerSm = 0;
   uint32_t nOut = 0;
+  const void* jitFn = nullptr;  // NVRTC kernel (cudaKernel_t) or null: interpreter
 
   ~PlanImpl() {
     int cur = 0;
@@ -128,6 +131,15 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   co.rewrite = opt.rewrite;
   I.prog = compileProgram(k, lits, sp, days, co);
   I.nOut = I.prog.header.n_instances * I.prog.header.n_days;
+  if (opt.jit < 0 || opt.jit > 2) throw UnsupportedError("unknown jit mode");
+  std::string jitSrc;
+  if (opt.jit != JIT_OFF) {
+    std::string why;
+    bool use = jitAvailable(&why);
+    if (use && opt.jit == JIT_AUTO && jitOpCount(I.prog) > kJitAutoMaxOps) use = false;
+    if (!use && opt.jit == JIT_ON) throw UnsupportedError("jit: " + why);
+    if (use) jitSrc = jitSource(I.prog);  // assigns steps[].jit_class (uploaded below)
+  }
 
   int dev = opt.device;
   if (dev < 0) ck(cudaGetDevice(&dev), "cudaGetDevice");
@@ -167,7 +179,15 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   if (I.smem > 227 * 1024)
     throw UnsupportedError("compiled payoff needs " + std::to_string(I.smem) +
                            " bytes of shared memory per CTA (max 232448)");
-  I.blocksPerSm = pathKernelOccupancy(I.prog.header, I.smem);
+  if (!jitSrc.empty()) {
+    I.jitFn = jitKernel(jitSrc);
+    ck(cudaFuncSetAttribute(I.jitFn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+       "jit cudaFuncSetAttribute");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&I.blocksPerSm, I.jitFn, kBlock, I.smem),
+       "jit occupancy");
+  } else {
+    I.blocksPerSm = pathKernelOccupancy(I.prog.header, I.smem);
+  }
   if (I.blocksPerSm <= 0) throw DeviceError("path kernel cannot be resident");
 }
 
@@ -191,6 +211,7 @@ PlanInfo Plan::info() const {
   r.block = kBlock;
   r.kernel_nodes = I.prog.kernelNodes;
   r.dag_nodes = I.prog.dagNodes;
+  r.jit = I.jitFn ? 1 : 0;
   return r;
 }
 
@@ -266,7 +287,13 @@ void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void*
   a.errKey = I.errKey;
   a.chunkCounter = I.chunkCounter;
   a.accScratch = I.accScratch;
-  ck(launchPath(I.dev, a, grid, I.smem, s), "path kernel launch");
+  if (I.jitFn) {
+    int accInSmem = I.accInSmem ? 1 : 0;
+    void* args[] = {&I.dev, &a, &accInSmem};
+    ck(cudaLaunchKernel(I.jitFn, dim3(grid), dim3(kBlock), args, I.smem, s), "jit path kernel launch");
+  } else {
+    ck(launchPath(I.dev, a, grid, I.smem, s), "path kernel launch");
+  }
 }
 
 std::vector<PriceResult> Plan::finalize(uint64_t paths, uint64_t seed, const void* partialsDev,

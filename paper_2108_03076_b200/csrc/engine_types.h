@@ -1,0 +1,67 @@
+// Launch-time types of the path kernel, shared by the host code, the
+// ahead-of-time device build and the NVRTC device build (no CUDA runtime
+// headers: NVRTC sees this file too).
+#pragma once
+#include <stdint.h>
+
+#include "program.h"
+
+namespace cltk {
+namespace b200 {
+
+constexpr int kBlock = 128;  // threads per CTA (4 warps)
+constexpr int kWarps = kBlock / 32;
+
+// Philox2x64-10 key schedule key_r = seed + r * 0x9E3779B97F4A7C15.
+struct PhiloxKeys {
+  uint64_t k[10];
+};
+#if !defined(__CUDACC_RTC__)
+inline PhiloxKeys philoxKeys(uint64_t seed) {
+  PhiloxKeys K;
+  for (int r = 0; r < 10; ++r) K.k[r] = seed + static_cast<uint64_t>(r) * 0x9E3779B97F4A7C15ULL;
+  return K;
+}
+#endif
+
+// Everything the path kernel reads, all device pointers.
+struct DevPlan {
+  cltk_plan_header hdr;
+  const cltk_step* steps;
+  const uint64_t* code;
+  const double* sharedConst;
+  const double* instConst;
+  const cltk_output* outputs;
+  // QMC mode
+  const cltk_bridge_op* bridge;
+  const uint32_t* sobolV;   // [2048][32] direction numbers
+  const uint32_t* sobolT5;  // [2048][32] XOR of v[d][0..4] over the set bits of g
+};
+
+struct RunArgs {
+  PhiloxKeys keys;
+  const uint32_t* sobolShift;  // QMC digital shift per dimension (null: none)
+  uint64_t seed;
+  uint64_t paths;        // total paths of the run (whole job, all GPUs)
+  uint64_t chunkPaths;   // kBlock * ppt
+  uint32_t ppt;          // paths per thread per chunk
+  uint64_t c0, c1;       // chunk range handled by this launch
+  cltk_partial* partials;           // [n_chunks][n_out]
+  unsigned long long* errKey;       // min(path << 24 | site)
+  unsigned long long* chunkCounter; // dynamic chunk scheduler
+  double* accScratch;               // global accumulators when n_out is large
+};
+
+// Dump modes (tests): per-path outputs instead of reduction.
+struct DumpArgs {
+  PhiloxKeys keys;
+  const uint32_t* sobolShift;
+  uint64_t seed, path0, npaths;
+  double* spots;    // [npaths][n_steps][n_assets] or null
+  double* outputs;  // [npaths][n_out] or null
+  double* normals;  // [npaths][n_steps][n_assets] or null
+  unsigned long long* errKey;
+};
+
+}  // namespace b200
+}  // namespace cltk

@@ -1,0 +1,345 @@
+// NVRTC code generation of compiled payoff programs (see jit.hpp).
+#include "jit.hpp"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <unordered_map>
+#include <vector>
+
+#include "engine_types.h"
+
+namespace cltk {
+namespace b200 {
+
+// Device sources embedded at build time (tools/embed_sources.py).
+extern const int kJitHeaderCount;
+extern const char* const kJitHeaderNames[];
+extern const char* const kJitHeaderSources[];
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// NVRTC, loaded on first use (the engine library does not link it).
+// ---------------------------------------------------------------------------
+struct Nvrtc {
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*,
+                        const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*logSize)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*cubinSize)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+  const char* (*errstr)(nvrtcResult) = nullptr;
+  std::string why;
+  bool ok = false;
+};
+
+Nvrtc loadNvrtc() {
+  Nvrtc n;
+  void* h = nullptr;
+  for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+    h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+    if (h) break;
+  }
+  if (!h) {
+    n.why = "libnvrtc.so.12 not loadable";
+    return n;
+  }
+  auto sym = [&](const char* s) { return dlsym(h, s); };
+  n.create = reinterpret_cast<decltype(n.create)>(sym("nvrtcCreateProgram"));
+  n.compile = reinterpret_cast<decltype(n.compile)>(sym("nvrtcCompileProgram"));
+  n.logSize = reinterpret_cast<decltype(n.logSize)>(sym("nvrtcGetProgramLogSize"));
+  n.log = reinterpret_cast<decltype(n.log)>(sym("nvrtcGetProgramLog"));
+  n.cubinSize = reinterpret_cast<decltype(n.cubinSize)>(sym("nvrtcGetCUBINSize"));
+  n.cubin = reinterpret_cast<decltype(n.cubin)>(sym("nvrtcGetCUBIN"));
+  n.destroy = reinterpret_cast<decltype(n.destroy)>(sym("nvrtcDestroyProgram"));
+  n.errstr = reinterpret_cast<decltype(n.errstr)>(sym("nvrtcGetErrorString"));
+  n.ok = n.create && n.compile && n.logSize && n.log && n.cubinSize && n.cubin && n.destroy &&
+         n.errstr;
+  if (!n.ok) n.why = "libnvrtc lacks the CUBIN API";
+  return n;
+}
+
+Nvrtc& nvrtc() {
+  static Nvrtc n = loadNvrtc();
+  return n;
+}
+
+// NVRTC has no C library headers: the engine headers only need these names.
+const char* kStdintStub =
+    "#pragma once\n"
+    "typedef unsigned long long uint64_t; typedef long long int64_t;\n"
+    "typedef unsigned int uint32_t; typedef int int32_t;\n"
+    "typedef unsigned short uint16_t; typedef short int16_t;\n"
+    "typedef unsigned char uint8_t; typedef signed char int8_t;\n";
+
+std::vector<uint8_t> compileCubin(const std::string& src, std::string* log) {
+  Nvrtc& n = nvrtc();
+  if (!n.ok) throw UnsupportedError("jit: " + n.why);
+  std::vector<const char*> names, bodies;
+  for (int i = 0; i < kJitHeaderCount; ++i) {
+    names.push_back(kJitHeaderNames[i]);
+    bodies.push_back(kJitHeaderSources[i]);
+  }
+  names.push_back("stdint.h");
+  bodies.push_back(kStdintStub);
+  names.push_back("math.h");
+  bodies.push_back("#pragma once\n");
+  nvrtcProgram prog;
+  nvrtcResult r = n.create(&prog, src.c_str(), "cltk_jit_path.cu", static_cast<int>(names.size()),
+                           bodies.data(), names.data());
+  if (r != NVRTC_SUCCESS) throw UnsupportedError(std::string("jit: nvrtc: ") + n.errstr(r));
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-fmad=false", "-lineinfo",
+                        "-DCLTK_JIT=1"};
+  r = n.compile(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
+  size_t ls = 0;
+  n.logSize(prog, &ls);
+  std::string lg(ls, '\0');
+  if (ls) n.log(prog, &lg[0]);
+  if (log) *log = lg;
+  if (r != NVRTC_SUCCESS) {
+    n.destroy(&prog);
+    throw UnsupportedError(std::string("jit: nvrtc compile failed: ") + n.errstr(r) + "\n" +
+                           lg.substr(0, 2000));
+  }
+  size_t cs = 0;
+  n.cubinSize(prog, &cs);
+  std::vector<uint8_t> cubin(cs);
+  n.cubin(prog, reinterpret_cast<char*>(cubin.data()));
+  n.destroy(&prog);
+  if (const char* dump = std::getenv("CLTK_JIT_DUMP")) {  // inspection: cuobjdump -sass
+    if (FILE* f = std::fopen(dump, "wb")) {
+      std::fwrite(cubin.data(), 1, cubin.size(), f);
+      std::fclose(f);
+    }
+  }
+  return cubin;
+}
+
+// ---------------------------------------------------------------------------
+// Code generation
+// ---------------------------------------------------------------------------
+struct DOp {
+  uint32_t op, d, a, b, c;
+};
+
+uint32_t fieldOf(uint64_t w, int sh) { return static_cast<uint32_t>(w >> sh) & 0x3fffu; }
+
+// The ops of packed[b, e) with VEC run headers expanded (run_ops semantics).
+std::vector<DOp> decode(const std::vector<uint64_t>& packed, uint32_t b, uint32_t e) {
+  std::vector<DOp> out;
+  for (uint32_t pc = b; pc < e;) {
+    const uint64_t w = packed[pc++];
+    const uint32_t op = static_cast<uint32_t>(w & 0xff);
+    if (op == OP_VEC) {
+      const uint32_t n = fieldOf(w, 8), vop = fieldOf(w, 22);
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint64_t u = packed[pc + i];
+        out.push_back({vop, fieldOf(u, 8), fieldOf(u, 22), fieldOf(u, 36), fieldOf(u, 50)});
+      }
+      pc += n;
+      continue;
+    }
+    out.push_back({op, fieldOf(w, 8), fieldOf(w, 22), fieldOf(w, 36), fieldOf(w, 50)});
+  }
+  return out;
+}
+
+bool usesA(uint32_t op) { return op != OP_NOP; }
+bool usesB(uint32_t op) {
+  switch (op) {
+    case OP_NOP: case OP_MOV: case OP_NEG: case OP_NOT: case OP_EDIVZ: return false;
+    default: return true;
+  }
+}
+
+// The expression of one op over locals a, b, c (run_ops in engine_device.cuh).
+std::string opExpr(const DOp& o) {
+  switch (o.op) {
+    case OP_MOV: return "a";
+    case OP_NEG: return "-a";
+    case OP_NOT: return "(a == 0.0 ? 1.0 : 0.0)";
+    case OP_ADD: return "__dadd_rn(a, b)";
+    case OP_SUB: return "__dsub_rn(a, b)";
+    case OP_MUL: return "__dmul_rn(a, b)";
+    case OP_DIV: return "__ddiv_rn(a, b)";
+    case OP_LT: return "(a < b ? 1.0 : 0.0)";
+    case OP_LEQ: return "(a <= b ? 1.0 : 0.0)";
+    case OP_EQ: return "(a == b ? 1.0 : 0.0)";
+    case OP_AND: return "((a != 0.0 && b != 0.0) ? 1.0 : 0.0)";
+    case OP_OR: return "((a != 0.0 || b != 0.0) ? 1.0 : 0.0)";
+    case OP_SEL: return "(a != 0.0 ? b : c)";
+    case OP_IADD:
+      return "of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(a)) + "
+             "static_cast<uint64_t>(bits_of(b))))";
+    case OP_ISUB:
+      return "of_bits(static_cast<int64_t>(static_cast<uint64_t>(bits_of(a)) - "
+             "static_cast<uint64_t>(bits_of(b))))";
+    case OP_ILT: return "(bits_of(a) < bits_of(b) ? 1.0 : 0.0)";
+    case OP_ILEQ: return "(bits_of(a) <= bits_of(b) ? 1.0 : 0.0)";
+    case OP_IEQ: return "(bits_of(a) == bits_of(b) ? 1.0 : 0.0)";
+    case OP_MIN: return "fmin(a, b)";
+    case OP_MAX: return "fmax(a, b)";
+    case OP_MINP:
+      return "((isnan(a) || isnan(b)) ? __longlong_as_double(0x7ff8000000000000LL) : fmin(a, b))";
+    case OP_MAXP:
+      return "((isnan(a) || isnan(b)) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(a, b))";
+    case OP_EFIRST: return "(bits_of(a) != 0 ? a : b)";
+    case OP_EDIVZ:
+      return "(a == 0.0 ? of_bits(static_cast<int64_t>(" + std::to_string(o.c) + "ll)) : 0.0)";
+    default: return "0.0";
+  }
+}
+
+struct Gen {
+  const CompiledProgram& prog;
+  uint32_t nA, nThread;
+  bool sRegs;
+
+  std::string opnd(uint32_t i, bool inStep) const {
+    if (i < nA && inStep && sRegs) return "S[" + std::to_string(i) + "]";
+    if (i < nThread) return "JR(" + std::to_string(i) + ")";
+    return "JC(" + std::to_string(i) + ")";
+  }
+  void emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep,
+            const char* ind) const {
+    for (const DOp& o : ops) {
+      if (o.op == OP_NOP) continue;
+      os << ind << "{ const double a = " << opnd(o.a, inStep) << ";";
+      if (usesB(o.op)) os << " const double b = " << opnd(o.b, inStep) << ";";
+      if (o.op == OP_SEL) os << " const double c = " << opnd(o.c, inStep) << ";";
+      os << " JW(" << o.d << ", " << opExpr(o) << "); }\n";
+    }
+  }
+};
+
+}  // namespace
+
+bool jitAvailable(std::string* why) {
+  Nvrtc& n = nvrtc();
+  if (!n.ok && why) *why = n.why;
+  return n.ok;
+}
+
+size_t jitOpCount(const CompiledProgram& prog) {
+  std::map<std::vector<uint64_t>, int> seen;
+  size_t n = 0;
+  for (const cltk_step& st : prog.steps) {
+    std::vector<uint64_t> key(prog.packed.begin() + st.code_begin,
+                              prog.packed.begin() + st.code_end);
+    if (key.empty() || seen.count(key)) continue;
+    seen[key] = 1;
+    n += decode(prog.packed, st.code_begin, st.code_end).size();
+  }
+  const cltk_plan_header& h = prog.header;
+  n += decode(prog.packed, h.inst_code_begin, h.inst_code_end).size();
+  return n;
+}
+
+std::string jitSource(CompiledProgram& prog) {
+  const cltk_plan_header& h = prog.header;
+  const uint32_t nA = h.n_assets ? h.n_assets : 1;
+  Gen g{prog, h.n_assets, h.n_thread, true};
+  // Spots come straight from registers unless something reads or writes the
+  // S-slots outside a step's own ops (then they are stored like the
+  // interpreter stores them).
+  const std::vector<DOp> instOps = decode(prog.packed, h.inst_code_begin, h.inst_code_end);
+  for (const DOp& o : instOps) {
+    if (o.op == OP_NOP) continue;
+    if (o.a < h.n_assets || (usesB(o.op) && o.b < h.n_assets) ||
+        (o.op == OP_SEL && o.c < h.n_assets) || o.d < h.n_assets)
+      g.sRegs = false;
+  }
+  for (const cltk_output& o : prog.outputs)
+    if (o.val < h.n_assets || (o.err != CLTK_NO_ERR && o.err < h.n_assets)) g.sRegs = false;
+  std::map<std::vector<uint64_t>, uint32_t> classes;
+  std::vector<std::vector<DOp>> classOps(1);
+  for (cltk_step& st : prog.steps) {
+    std::vector<uint64_t> key(prog.packed.begin() + st.code_begin,
+                              prog.packed.begin() + st.code_end);
+    if (key.empty()) {
+      st.jit_class = 0;
+      continue;
+    }
+    auto it = classes.find(key);
+    if (it == classes.end()) {
+      const uint32_t id = static_cast<uint32_t>(classOps.size());
+      it = classes.emplace(key, id).first;
+      classOps.push_back(decode(prog.packed, st.code_begin, st.code_end));
+      for (const DOp& o : classOps.back())
+        if (o.op != OP_NOP && o.d < h.n_assets) g.sRegs = false;
+    }
+    st.jit_class = it->second;
+  }
+  std::ostringstream os;
+  os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
+        "#define CLTK_JIT 1\n"
+        "#include \"engine_device.cuh\"\n"
+        "namespace cltk {\nnamespace b200 {\nnamespace {\n"
+        "static_assert(sizeof(DevPlan) == "
+     << sizeof(DevPlan) << ", \"DevPlan layout\");\nstatic_assert(sizeof(RunArgs) == "
+     << sizeof(RunArgs) << ", \"RunArgs layout\");\nstatic_assert(sizeof(cltk_step) == "
+     << sizeof(cltk_step)
+     << ", \"cltk_step layout\");\n"
+        "#define JR(i) lds64(f.R + (i) * (kBlock * 8u))\n"
+        "#define JW(i, v) sts64(f.R + (i) * (kBlock * 8u), (v))\n"
+        "#define JC(i) lds64(f.C + (i) * 8u)\n"
+        "struct JitPayoff {\n"
+        "  template <int NA>\n"
+        "  static __device__ __forceinline__ void step(const Frame f, const DevPlan& P,\n"
+        "                                              const cltk_step* st, const double (&S)[NA]) {\n"
+        "    switch (__ldg(&st->jit_class)) {\n";
+  for (size_t c = 1; c < classOps.size(); ++c) {
+    os << "      case " << c << ": {\n";
+    if (!g.sRegs)
+      for (uint32_t j = 0; j < h.n_assets; ++j) os << "        JW(" << j << ", S[" << j << "]);\n";
+    g.emit(os, classOps[c], true, "        ");
+    os << "        break;\n      }\n";
+  }
+  os << "      default: break;\n    }\n  }\n"
+        "  static __device__ __forceinline__ void inst(const Frame f, const DevPlan& P) {\n";
+  g.emit(os, instOps, false, "    ");
+  os << "  }\n};\n}  // namespace\n}  // namespace b200\n}  // namespace cltk\n"
+        "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, CLTK_MIN_BLOCKS)\n"
+        "cltk_jit_path(const cltk::b200::DevPlan P, const cltk::b200::RunArgs A, int accInSmem) {\n"
+        "  cltk::b200::path_body<"
+     << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false")
+     << ", cltk::b200::JitPayoff>(P, A, accInSmem);\n}\n";
+  return os.str();
+}
+
+size_t jitCompileOnly(const std::string& src, std::string* log) {
+  return compileCubin(src, log).size();
+}
+
+const void* jitKernel(const std::string& src) {
+  static std::mutex mu;
+  static std::unordered_map<std::string, cudaKernel_t> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(src);
+  if (it != cache.end()) return reinterpret_cast<const void*>(it->second);
+  std::string log;
+  std::vector<uint8_t> cubin = compileCubin(src, &log);
+  cudaLibrary_t lib;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess)
+    throw DeviceError(std::string("jit: cudaLibraryLoadData: ") + cudaGetErrorString(e));
+  cudaKernel_t k;
+  e = cudaLibraryGetKernel(&k, lib, "cltk_jit_path");
+  if (e != cudaSuccess)
+    throw DeviceError(std::string("jit: cudaLibraryGetKernel: ") + cudaGetErrorString(e));
+  cache.emplace(src, k);
+  return reinterpret_cast<const void*>(k);
+}
+
+}  // namespace b200
+}  // namespace cltk

@@ -59,12 +59,14 @@ enum cltk_opcode : uint32_t {
   OP_VEC = 63
 };
 
+#if !defined(__CUDACC_RTC__)
 // 64-bit instruction: op | d<<8 | a<<22 | b<<36 | c<<50
 static inline uint64_t cltk_encode(uint32_t op, uint32_t d, uint32_t a,
                                    uint32_t b, uint32_t c) {
   return (uint64_t)op | ((uint64_t)d << 8) | ((uint64_t)a << 22) |
          ((uint64_t)b << 36) | ((uint64_t)c << 50);
 }
+#endif
 
 // Per-step simulation constants (host-computed with glibc, bit-identical to
 // the reference's SimPlan arithmetic, proj/src/pricing.cpp:226-245).
@@ -81,6 +83,9 @@ typedef struct {
   uint32_t br_begin;
   uint32_t br_end;
   uint32_t br_emit;
+  // NVRTC mode: the step's op class (steps with identical ops share one;
+  // 0 = no ops), the `case` of the generated payoff policy (jit.cpp).
+  uint32_t jit_class;
 } cltk_step;
 
 // Brownian-bridge construction op (QMC mode): for every asset j

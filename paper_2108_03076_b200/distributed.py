@@ -57,14 +57,14 @@ class DistributedPricer:
 
     def __init__(self, kernels: Sequence[Kernel] | Kernel, model, days: Sequence[int] = (0,),
                  tenv: dict | None = None, device: int | None = None, rewrite: bool = True,
-                 literals=None, rng: str = "philox"):
+                 literals=None, rng: str = "philox", jit=False):
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         if device is None:
             device = torch.cuda.current_device()
         self.device = device
         self.plan = Plan(kernels, model, days, tenv, device=device, rewrite=rewrite,
-                         literals=literals, rng=rng)
+                         literals=literals, rng=rng, jit=jit)
         self._parts = None
         self._paths = None
 
@@ -99,6 +99,7 @@ class DistributedPricer:
 
 def price(kernel: Kernel | Sequence[Kernel], model, paths: int = 100000, seed: int = 0,
           days: Sequence[int] = (0,), tenv: dict | None = None, literals=None,
-          rng: str = "philox") -> list[dict]:
+          rng: str = "philox", jit=False) -> list[dict]:
     """priceAcrossTime over every rank of the default process group."""
-    return DistributedPricer(kernel, model, days, tenv, literals=literals, rng=rng).price(paths, seed)
+    return DistributedPricer(kernel, model, days, tenv, literals=literals, rng=rng,
+                             jit=jit).price(paths, seed)

@@ -1,0 +1,134 @@
+"""NVRTC payoff kernels (csrc/jit.cpp): the compiled payoff program emitted as
+CUDA and built for sm_100a at plan creation.
+
+CPU: every golden contract's generated source NVRTC-compiles for sm_100a (no
+device needed) and the generator's structure (step classes, spots from
+registers, literals as kernel data).
+GPU: prices through the NVRTC kernel equal the interpreter's bit for bit --
+same ops, same order, same IEEE operations -- for every golden case, both RNG
+modes, template batches and literal tables, and the error channel.
+"""
+import re
+
+import numpy as np
+import pytest
+
+import paper_2108_03076_b200 as E
+from conftest import load_cases, load_kernel, load_model
+
+CASES = load_cases()
+
+
+def _case(name):
+    return next(x for x in CASES if x["name"] == name)
+
+
+@pytest.mark.parametrize("kern,model,days,tenv", [
+    ("european-call", "call", [0, 45], {}),
+    ("barrier", "barrier", [0, 10], {}),
+    ("double-option", "double", [0, 30, 45], {}),
+    ("fx-swap", "fx", [0, 30, 60, 90], {}),
+    ("template-option", "call", [0, 10, 50], {"t0": 10, "t1": 80}),
+    ("worst-off", "three", [0, 100], {}),
+    ("brc", "three", [0, 180], {}),
+])
+def test_generated_source_compiles_for_sm100a(kern, model, days, tenv):
+    src = E.jit_source(E.Kernel(load_kernel(kern)), load_model(model), days, tenv)
+    assert "cltk_jit_path" in src and "path_body<" in src
+    n, log = E.jit_compile(src)
+    assert n > 0, log
+
+
+def test_brc_source_structure():
+    """BRC 3 x 367: 365 identical running-min steps share one class; the spots
+    are read from registers; the barrier/strike literals are table operands
+    (JC), never baked in (new literal values reuse the compiled kernel)."""
+    k = E.Kernel(load_kernel("brc"))
+    m = load_model("three")
+    src = E.jit_source(k, m, [0])
+    cases = re.findall(r"case (\d+): \{", src)
+    assert len(cases) == 3, cases
+    assert "S[0]" in src and "fmin(a, b)" in src
+    for lit in ("2630.635", "8288", "840"):
+        assert lit not in src
+    # a different literal instance of the template: identical source
+    lo = k.with_literals({2630.635: 1879.0, 8288.0: 5920.0, 840.0: 600.0})
+    assert E.jit_source(lo, m, [0]) == src
+    sobol = E.jit_source(k, m, [0], rng="sobol")
+    assert "path_body<3, true" in sobol and "path_body<3, false" in src
+
+
+def test_jit_modes_validated():
+    with pytest.raises(ValueError):
+        E.price(E.Kernel(load_kernel("european-call")), load_model("call"), 10, 1, jit="yes")
+
+
+def _bits(rs):
+    return [(float(r["price"]).hex(), float(r["std_error"]).hex()) for r in rs]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c["name"] for c in CASES])
+def test_jit_prices_equal_interpreter_bitwise(case):
+    c = _case(case)
+    k, m = E.Kernel(load_kernel(c["kernel"])), load_model(c["model"])
+    n = 50_000 if c["kernel"] != "brc" else 20_000
+    a = E.price(k, m, n, c["seed"], c["days"], c["tenv"])
+    b = E.price(k, m, n, c["seed"], c["days"], c["tenv"], jit=True)
+    assert _bits(a) == _bits(b)
+
+
+@pytest.mark.gpu
+def test_jit_plan_reports_nvrtc_and_matches_reference_case():
+    c = _case("worst_off_days")
+    k, m = E.Kernel(load_kernel(c["kernel"])), load_model(c["model"])
+    plan = E.Plan(k, m, c["days"], jit=True)
+    assert plan.info["jit"] == 1
+    assert E.Plan(k, m, c["days"]).info["jit"] == 0
+    assert E.Plan(k, m, c["days"], jit="auto").info["jit"] == 1
+    # the reference's own prices at the golden path counts (summation order only)
+    for pr in c["prices"]:
+        got = E.price(k, m, pr["paths"], c["seed"], c["days"], jit=True)
+        for g, p in zip(got, pr["price"]):
+            P = float.fromhex(p)
+            assert abs(g["price"] - P) <= 1e-13 * abs(P) + 1e-13, (g["price"], P)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kern,model", [("brc", "three"), ("worst-off", "three"),
+                                        ("european-call", "call")])
+def test_jit_qmc_equals_interpreter_bitwise(kern, model):
+    k, m = E.Kernel(load_kernel(kern)), load_model(model)
+    a = E.price(k, m, 40_000, 3, [0], rng="sobol")
+    b = E.price(k, m, 40_000, 3, [0], rng="sobol", jit=True)
+    assert _bits(a) == _bits(b)
+
+
+@pytest.mark.gpu
+def test_jit_template_batch_and_literal_table_bitwise():
+    brc = E.Kernel(load_kernel("brc"))
+    m = load_model("three")
+    insts = [brc.with_literals({2630.635: 3758.05 * f, 8288.0: 11840.0 * f, 840.0: 1200.0 * f})
+             for f in (0.5, 0.7, 0.9)]
+    a = E.price_batch(insts, m, 20_000, 42)
+    b = E.price_batch(insts, m, 20_000, 42, jit=True)
+    assert [_bits(x) for x in a] == [_bits(x) for x in b]
+    lits = np.array([E.kernel_literals(x) for x in insts])
+    c = E.price_template(brc, lits, m, 20_000, 42, jit=True)
+    assert [_bits(x) for x in c] == [_bits(x) for x in a]
+
+
+@pytest.mark.gpu
+def test_jit_division_by_zero_raises_like_interpreter():
+    kern = {"body": {"kind": "binop", "op": "div", "left": {"kind": "float", "value": 1.0},
+                     "right": {"kind": "binop", "op": "sub",
+                               "left": {"kind": "obsref", "row": 0, "col": 0},
+                               "right": {"kind": "obsref", "row": 0, "col": 0}}},
+            "rows": [5], "cols": ["AAPL"], "tvars": [], "parties": [], "horizon": 6}
+    with pytest.raises(E.ContractError, match="kernel: division by zero") as ei:
+        E.price(E.Kernel(kern), load_model("call"), 1000, 1, jit=True)
+    assert ei.value.code == 5
+    safe = {"body": {"kind": "if", "cond": {"kind": "bool", "value": False},
+                     "then": kern["body"], "else": {"kind": "float", "value": 2.0}},
+            "rows": [5], "cols": ["AAPL"], "tvars": [], "parties": [], "horizon": 6}
+    assert E.price(E.Kernel(safe), load_model("call"), 1000, 1, jit=True)[0]["price"] == 2.0

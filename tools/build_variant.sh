@@ -12,4 +12,4 @@ make -s lib >/dev/null
 grep -A3 "Compiling entry.*path_kernelILi3ELb0" $d/ptxas.txt | tail -2 | tr -s ' ' | sed "s|^|$name: |"
 objs=$(ls build/obj/*.o | grep -v mc_engine)
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -ccbin /usr/bin/g++ -cudart static \
-  -o $d/libcltk_b200.so $objs $d/mc_engine.o
+  -o $d/libcltk_b200.so $objs $d/mc_engine.o -ldl
