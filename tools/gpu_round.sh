@@ -16,14 +16,14 @@ timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref
 M=smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,gpu__time_duration.sum
 for w in worst_off call; do
   CMD="python bench.py --workload $w --steps 1 --warmup 1 --paths-per-gpu 2000000 --e2e-steps 0 --no-cpu-baseline"
-  $CMD > $O/plain_$w.log 2>&1 && ncu --metrics $M --clock-control none -k regex:path_kernel -s 1 -c 1 --csv --log-file $O/fp64ops_$w.csv $CMD > $O/ncu_$w.log 2>&1
+  $CMD > $O/plain_$w.log 2>&1 && ncu --metrics $M --clock-control none -k regex:path -s 1 -c 1 --csv --log-file $O/fp64ops_$w.csv $CMD > $O/ncu_$w.log 2>&1
 done
 if [ "${1:-}" = "full" ]; then
   # launch list of the default bench command (per-launch times, cold-cache, serialised)
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > $O/ncu_launches.log 2>&1
   # one full capture of the hot kernel (smaller step so the ~40 replays stay short)
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 3 -c 1 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:path -s 3 -c 1 \
     -o $O/brc_full python bench.py --steps 1 --warmup 3 --paths-per-gpu 10000000 --e2e-steps 0 --no-cpu-baseline > $O/ncu_full.log 2>&1
 fi
 echo done

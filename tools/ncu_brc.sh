@@ -4,6 +4,6 @@ name=${1:-brc_full}
 paths=${2:-10000000}
 CMD="python bench.py --steps 1 --warmup 3 --paths-per-gpu $paths --e2e-steps 0 --no-cpu-baseline"
 $CMD > gpurun_out/${name}_plain.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 3 -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:path -s 3 -c 1 \
   -o gpurun_out/$name $CMD > gpurun_out/${name}_ncu.log 2>&1
 echo "ncu rc=$?"
