@@ -98,9 +98,15 @@ std::vector<uint8_t> compileCubin(const std::string& src, std::string* log) {
   nvrtcResult r = n.create(&prog, src.c_str(), "cltk_jit_path.cu", static_cast<int>(names.size()),
                            bodies.data(), names.data());
   if (r != NVRTC_SUCCESS) throw UnsupportedError(std::string("jit: nvrtc: ") + n.errstr(r));
-  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-fmad=false", "-lineinfo",
-                        "-DCLTK_JIT=1"};
-  r = n.compile(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
+  std::vector<std::string> extra;  // CLTK_JIT_FLAGS: extra NVRTC options (experiments)
+  if (const char* f = std::getenv("CLTK_JIT_FLAGS")) {
+    std::istringstream is(f);
+    for (std::string t; is >> t;) extra.push_back(t);
+  }
+  std::vector<const char*> opts = {"-arch=sm_100a", "-std=c++17", "-fmad=false", "-lineinfo",
+                                   "-DCLTK_JIT=1"};
+  for (const std::string& t : extra) opts.push_back(t.c_str());
+  r = n.compile(prog, static_cast<int>(opts.size()), opts.data());
   size_t ls = 0;
   n.logSize(prog, &ls);
   std::string lg(ls, '\0');
@@ -280,6 +286,8 @@ std::string jitSource(CompiledProgram& prog) {
     }
     st.jit_class = it->second;
   }
+  // S-slots in registers: no shared-memory columns for them
+  prog.header.reg_base = g.sRegs ? h.n_assets : 0;
   std::ostringstream os;
   os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
         "#define CLTK_JIT 1\n"

@@ -65,7 +65,8 @@ bool accFitsSmem(const cltk_plan_header& h) {
 
 size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
   const size_t nOut = static_cast<size_t>(h.n_instances) * h.n_days;
-  size_t words = static_cast<size_t>(h.n_thread) * kBlock + kWarps * (h.n_shared_const + h.n_inst_const);
+  size_t words = static_cast<size_t>(h.n_thread - h.reg_base) * kBlock +
+                 kWarps * (h.n_shared_const + h.n_inst_const);
   if (accInSmem) words += kWarps * nOut * 3;
   words += kWarps + 1;  // counts + chunk slot
   words += kNormScratchWords;

@@ -114,7 +114,8 @@ typedef struct {
   uint32_t rng;             // CLTK_RNG_PHILOX (reference parity) / CLTK_RNG_SOBOL
   uint32_t n_bridge_slots;  // QMC: W slots per asset
   uint32_t n_bridge_ops;    // QMC: computes (= drawing steps)
-  uint32_t pad;
+  uint32_t reg_base;        // path kernel: leading operand slots without shared-memory
+                            // columns (the NVRTC kernel keeps the S-slots in registers)
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
