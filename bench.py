@@ -341,7 +341,7 @@ def main():
                            "kernel_ms": t_kern},
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": paths * n_inst / t_e2e if t_e2e > 0 else None, "unit": "paths/s",
-                        "h2d_bytes_per_step": h2d,
+                        "h2d_bytes_per_step": h2d, "samples_ms": [round(t * 1e3, 3) for t in e2e_times],
                         "d2h_bytes_per_step": d2h,
                         "path": "paper_2108_03076_b200.price -> cltk_gpu_price[_ex] (C-ABI), host "
                                 "kernel/model JSON in, host results out"},
