@@ -210,10 +210,15 @@ struct Gen {
   const CompiledProgram& prog;
   uint32_t nA, nThread;
   bool sRegs;
+  bool copyInst = false;  // something outside inst() reads the instance literal pool
+  uint32_t nc = 0, ni = 0;
 
   std::string opnd(uint32_t i, bool inStep) const {
     if (i < nA && inStep && sRegs) return "S[" + std::to_string(i) + "]";
     if (i < nThread) return "JR(" + std::to_string(i) + ")";
+    // instance literals straight from the table (L1-resident, warp-broadcast)
+    if (!copyInst && i >= nThread + nc && i < nThread + nc + ni)
+      return "JI(" + std::to_string(i - nThread - nc) + ")";
     return "JC(" + std::to_string(i) + ")";
   }
   void emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep,
@@ -265,8 +270,15 @@ std::string jitSource(CompiledProgram& prog) {
         (o.op == OP_SEL && o.c < h.n_assets) || o.d < h.n_assets)
       g.sRegs = false;
   }
-  for (const cltk_output& o : prog.outputs)
+  g.nc = h.n_shared_const;
+  g.ni = h.n_inst_const;
+  const uint32_t instLo = h.n_thread + h.n_shared_const, instHi = instLo + h.n_inst_const;
+  for (const cltk_output& o : prog.outputs) {
     if (o.val < h.n_assets || (o.err != CLTK_NO_ERR && o.err < h.n_assets)) g.sRegs = false;
+    if ((o.val >= instLo && o.val < instHi) ||
+        (o.err != CLTK_NO_ERR && o.err >= instLo && o.err < instHi))
+      g.copyInst = true;
+  }
   std::map<std::vector<uint64_t>, uint32_t> classes;
   std::vector<std::vector<DOp>> classOps(1);
   for (cltk_step& st : prog.steps) {
@@ -301,7 +313,10 @@ std::string jitSource(CompiledProgram& prog) {
         "#define JR(i) lds64(f.R + (i) * (kBlock * 8u))\n"
         "#define JW(i, v) sts64(f.R + (i) * (kBlock * 8u), (v))\n"
         "#define JC(i) lds64(f.C + (i) * 8u)\n"
+        "#define JI(k) __ldg(P.instConst + static_cast<size_t>(inst) * P.hdr.n_inst_const + (k))\n"
         "struct JitPayoff {\n"
+        "  static constexpr bool kCopyInstConst = "
+     << (g.copyInst ? "true" : "false") << ";\n"
         "  template <int NA>\n"
         "  static __device__ __forceinline__ void step(const Frame f, const DevPlan& P,\n"
         "                                              const cltk_step* st, const double (&S)[NA]) {\n"
@@ -314,7 +329,8 @@ std::string jitSource(CompiledProgram& prog) {
     os << "        break;\n      }\n";
   }
   os << "      default: break;\n    }\n  }\n"
-        "  static __device__ __forceinline__ void inst(const Frame f, const DevPlan& P) {\n";
+        "  static __device__ __forceinline__ void inst(const Frame f, const DevPlan& P,\n"
+        "                                              uint32_t inst) {\n";
   g.emit(os, instOps, false, "    ");
   os << "  }\n};\n}  // namespace\n}  // namespace b200\n}  // namespace cltk\n"
         "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, CLTK_MIN_BLOCKS)\n"
