@@ -173,9 +173,11 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
                          const char* tenv_json, int rewrite, int rng, char** json,
                          cltk_error* err);
 /* Host-only: the CUDA source the NVRTC mode generates for this program
- * (malloc'd; free with cltk_free).  Replaces no reference interface (the
+ * (literals: an optional [n_instances][n_literals] table as in
+ * cltk_plan_create_ex; malloc'd; free with cltk_free).  Replaces no reference interface (the
  * reference interprets its kernel tree, proj/src/kernel.cpp:229-310). */
-int cltk_jit_source(const char* kernel_json, const char* model_json, const uint64_t* days,
+int cltk_jit_source(const char* kernel_json, const double* literals, size_t n_instances,
+                    size_t n_literals, const char* model_json, const uint64_t* days,
                     size_t n_days, const char* tenv_json, int rewrite, int rng, char** source,
                     cltk_error* err);
 /* Host-only: NVRTC-compile a generated source for sm_100a (no device needed);

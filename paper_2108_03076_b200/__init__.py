@@ -337,14 +337,23 @@ def compile_listing(kernels: Sequence[Kernel | str | dict] | Kernel, model: str 
 
 
 def jit_source(kernel: Kernel | str | dict, model: str | dict, days: Sequence[int] = (0,),
-               tenv: dict | None = None, rewrite: bool = True, rng: str = "philox") -> str:
-    """Host-only: the CUDA source of the NVRTC payoff kernel for this program."""
+               tenv: dict | None = None, rewrite: bool = True, rng: str = "philox",
+               literals=None) -> str:
+    """Host-only: the CUDA source of the NVRTC payoff kernel for this program
+    (``literals``: optional template literal table, as in ``price_template``)."""
+    import numpy as np
     L = _native.lib()
     d, nd = _days(days)
     out = C.c_void_p()
     err = _native.ErrorC()
-    rc = L.cltk_jit_source(_kernel_json(kernel), _model_json(model), d, nd, _tenv_json(tenv),
-                           int(rewrite), RNG_MODES[rng], C.byref(out), C.byref(err))
+    if literals is not None:
+        lit = np.ascontiguousarray(literals, dtype=np.float64)
+        lp, n_i, n_l = lit.ctypes.data, lit.shape[0], lit.shape[1]
+    else:
+        lit, lp, n_i, n_l = None, None, 1, 0
+    rc = L.cltk_jit_source(_kernel_json(kernel), lp, n_i, n_l, _model_json(model), d, nd,
+                           _tenv_json(tenv), int(rewrite), RNG_MODES[rng], C.byref(out),
+                           C.byref(err))
     _raise(rc, err)
     s = C.cast(out, C.c_char_p).value.decode()
     L.cltk_free(out)

@@ -104,7 +104,8 @@ def lib() -> C.CDLL:
     L.cltk_plan_create_ex.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t, cp, PO,
                                       C.POINTER(vp), PE]
     L.cltk_jit_source.restype = i32
-    L.cltk_jit_source.argtypes = [cp, cp, P64, C.c_size_t, cp, i32, i32, C.POINTER(vp), PE]
+    L.cltk_jit_source.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t, cp, i32, i32,
+                                  C.POINTER(vp), PE]
     L.cltk_jit_compile.restype = i32
     L.cltk_jit_compile.argtypes = [cp, P64, C.POINTER(vp), PE]
     L.cltk_plan_create_batch_ex.restype = i32

@@ -351,7 +351,8 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
   });
 }
 
-int cltk_jit_source(const char* kernel_json, const char* model_json, const uint64_t* days,
+int cltk_jit_source(const char* kernel_json, const double* literals, size_t n_instances,
+                    size_t n_literals, const char* model_json, const uint64_t* days,
                     size_t n_days, const char* tenv_json, int rewrite, int rng, char** source,
                     cltk_error* err) {
   return guarded(err, [&] {
@@ -362,8 +363,18 @@ int cltk_jit_source(const char* kernel_json, const char* model_json, const uint6
     for (const auto& v : k.tvars) (void)t.lookup(v);
     CompileOptions co;
     co.rewrite = rewrite != 0;
-    std::vector<const Kernel*> ptrs{&k};
-    CompiledProgram P = compileProgram(ptrs, sp, std::vector<uint64_t>(days, days + n_days), co);
+    LiteralTable lits;
+    if (literals) {
+      lits.nInst = n_instances;
+      lits.nOcc = n_literals;
+      lits.values.assign(literals, literals + n_instances * n_literals);
+    } else {
+      lits.values = kernelFloatLiterals(k);
+      lits.nInst = 1;
+      lits.nOcc = lits.values.size();
+    }
+    CompiledProgram P =
+        compileProgram(k, lits, sp, std::vector<uint64_t>(days, days + n_days), co);
     const std::string src = jitSource(P);
     char* p = static_cast<char*>(std::malloc(src.size() + 1));
     std::memcpy(p, src.c_str(), src.size() + 1);

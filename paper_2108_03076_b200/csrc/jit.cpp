@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <sstream>
 #include <unordered_map>
 #include <vector>
@@ -221,14 +222,75 @@ struct Gen {
       return "JI(" + std::to_string(i - nThread - nc) + ")";
     return "JC(" + std::to_string(i) + ")";
   }
-  void emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep,
-            const char* ind) const {
+  // Readers of each thread register outside a given block: other blocks, the
+  // outputs.  Block ids: step classes 1..C, the instance section C + 1.
+  std::map<uint32_t, std::set<uint32_t>> readBy;
+  std::set<uint32_t> outRead;
+
+  void noteReads(const std::vector<DOp>& ops, uint32_t block) {
     for (const DOp& o : ops) {
       if (o.op == OP_NOP) continue;
-      os << ind << "{ const double a = " << opnd(o.a, inStep) << ";";
-      if (usesB(o.op)) os << " const double b = " << opnd(o.b, inStep) << ";";
-      if (o.op == OP_SEL) os << " const double c = " << opnd(o.c, inStep) << ";";
-      os << " JW(" << o.d << ", " << opExpr(o) << "); }\n";
+      if (o.a < nThread) readBy[o.a].insert(block);
+      if (usesB(o.op) && o.b < nThread) readBy[o.b].insert(block);
+      if (o.op == OP_SEL && o.c < nThread) readBy[o.c].insert(block);
+    }
+  }
+
+  // Straight-line emission of one block with its values in locals: a register
+  // is loaded from its shared-memory column at its first read in the block (if
+  // not yet written there), every op result is a new local, and at the end a
+  // register is stored back only if something outside the block can read it
+  // (another block, the outputs, or this block's next occurrence -- a read
+  // before the write).  Same ops, same order, same IEEE operations.
+  void emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep, uint32_t block,
+            const char* ind) const {
+    std::map<uint32_t, std::string> cur;
+    std::set<uint32_t> dirty, carried;
+    int n = 0;
+    if (inStep && !sRegs)
+      for (uint32_t j = 0; j < nA; ++j) {
+        cur[j] = "S[" + std::to_string(j) + "]";
+        dirty.insert(j);
+      }
+    auto val = [&](uint32_t i) -> std::string {
+      if (i < nA && inStep && sRegs) return "S[" + std::to_string(i) + "]";
+      auto it = cur.find(i);
+      if (it != cur.end()) return it->second;
+      const std::string v = "v" + std::to_string(n++);
+      std::string src;
+      if (i < nThread) {
+        carried.insert(i);
+        src = "JR(" + std::to_string(i) + ")";
+      } else if (!copyInst && i >= nThread + nc && i < nThread + nc + ni) {
+        // instance literals straight from the table (L1-resident, broadcast)
+        src = "JI(" + std::to_string(i - nThread - nc) + ")";
+      } else {
+        src = "JC(" + std::to_string(i) + ")";
+      }
+      os << ind << "const double " << v << " = " << src << ";\n";
+      cur[i] = v;
+      return v;
+    };
+    for (const DOp& o : ops) {
+      if (o.op == OP_NOP) continue;
+      const std::string a = val(o.a);
+      const std::string b = usesB(o.op) ? val(o.b) : std::string();
+      const std::string c = o.op == OP_SEL ? val(o.c) : std::string();
+      const std::string t = "v" + std::to_string(n++);
+      os << ind << "double " << t << ";\n" << ind << "{ const double a = " << a << ";";
+      if (!b.empty()) os << " const double b = " << b << ";";
+      if (!c.empty()) os << " const double c = " << c << ";";
+      os << " " << t << " = " << opExpr(o) << "; }\n";
+      cur[o.d] = t;
+      dirty.insert(o.d);
+    }
+    for (uint32_t r : dirty) {
+      bool live = outRead.count(r) || carried.count(r);
+      auto it = readBy.find(r);
+      if (!live && it != readBy.end())
+        for (uint32_t bl : it->second)
+          if (bl != block) live = true;
+      if (live) os << ind << "JW(" << r << ", " << cur[r] << ");\n";
     }
   }
 };
@@ -300,6 +362,13 @@ std::string jitSource(CompiledProgram& prog) {
   }
   // S-slots in registers: no shared-memory columns for them
   prog.header.reg_base = g.sRegs ? h.n_assets : 0;
+  const uint32_t instBlock = static_cast<uint32_t>(classOps.size());
+  for (size_t c = 1; c < classOps.size(); ++c) g.noteReads(classOps[c], static_cast<uint32_t>(c));
+  g.noteReads(instOps, instBlock);
+  for (const cltk_output& o : prog.outputs) {
+    if (o.val < h.n_thread) g.outRead.insert(o.val);
+    if (o.err != CLTK_NO_ERR && o.err < h.n_thread) g.outRead.insert(o.err);
+  }
   std::ostringstream os;
   os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
         "#define CLTK_JIT 1\n"
@@ -323,15 +392,13 @@ std::string jitSource(CompiledProgram& prog) {
         "    switch (__ldg(&st->jit_class)) {\n";
   for (size_t c = 1; c < classOps.size(); ++c) {
     os << "      case " << c << ": {\n";
-    if (!g.sRegs)
-      for (uint32_t j = 0; j < h.n_assets; ++j) os << "        JW(" << j << ", S[" << j << "]);\n";
-    g.emit(os, classOps[c], true, "        ");
+    g.emit(os, classOps[c], true, static_cast<uint32_t>(c), "        ");
     os << "        break;\n      }\n";
   }
   os << "      default: break;\n    }\n  }\n"
         "  static __device__ __forceinline__ void inst(const Frame f, const DevPlan& P,\n"
         "                                              uint32_t inst) {\n";
-  g.emit(os, instOps, false, "    ");
+  g.emit(os, instOps, false, instBlock, "    ");
   os << "  }\n};\n}  // namespace\n}  // namespace b200\n}  // namespace cltk\n"
         "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, CLTK_MIN_BLOCKS)\n"
         "cltk_jit_path(const cltk::b200::DevPlan P, const cltk::b200::RunArgs A, int accInSmem) {\n"
