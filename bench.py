@@ -31,7 +31,8 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 # FP64 flops per path of the fused kernel, frozen from the ncu SASS op counters
 # (dadd + dmul + 2*dfma) of the first correct kernel (profiles/).
-F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None}
+F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None,
+          "worst_off_batch": None}
 # brc: ncu r1 (profiles/r1_path_kernel_brc_2M_raw.csv), 2e6 paths:
 #   dadd 6.2471e10 + dmul 7.0817e10 + 2 * dfma 2.19577e11 thread-instructions
 # worst_off / call: first measurement (profiles/r1_fp64ops_*_2M.csv), 2e6 paths
@@ -39,20 +40,25 @@ F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None
 BATCH_N = 1024
 
 
-def batch_literals(kern_json: str):
-    """C4: 1024 instances of the BRC template -- knock-in barrier at 50%..80%
-    of spot and strike at 90%..110% of spot, in the literal pool only."""
+def batch_literals(kern_json: str, workload: str = "brc_batch"):
+    """C4: 1024 instances of one template, literal pool only.  BRC: knock-in
+    barrier at 50%..80% of spot and strike at 90%..110% of spot; worst-off:
+    knock-in level 0.50..0.80 and autocall trigger 0.90..1.10."""
     import paper_2108_03076_b200 as E
     base = E.kernel_literals(kern_json)
-    spots = {3758.05: 2630.635, 11840.0: 8288.0, 1200.0: 840.0}  # spot -> 70% barrier
     rows = []
     for i in range(BATCH_N):
         b = 0.5 + 0.3 * i / (BATCH_N - 1)
         r = 0.9 + 0.2 * ((i * 389) % BATCH_N) / (BATCH_N - 1)
         sub = {}
-        for sp, bar in spots.items():
-            sub[bar] = sp * b
-            sub[sp] = sp * r
+        if workload == "brc_batch":
+            spots = {3758.05: 2630.635, 11840.0: 8288.0, 1200.0: 840.0}  # spot -> 70% barrier
+            for sp, bar in spots.items():
+                sub[bar] = sp * b
+                sub[sp] = sp * r
+        else:
+            sub[0.75] = b
+            sub[1.0] = r
         rows.append([sub.get(v, v) for v in base])
     return rows
 
@@ -60,6 +66,8 @@ def batch_literals(kern_json: str):
 WORKLOADS = {
     "brc_batch": ("brc", "three", f"C4: {BATCH_N} instances of the BRC template (barrier "
                   "50-80%, strike 90-110% of spot) on one path set, literals as kernel data"),
+    "worst_off_batch": ("worst-off", "three", f"C4: {BATCH_N} instances of the worst-off template "
+                        "(knock-in 0.50-0.80, autocall trigger 0.90-1.10) on one path set"),
     "brc": ("brc", "three", "BRC 3 underlyings x 367 dates (contracts/brc.cl, SURVEY.md App. A)"),
     "worst_off": ("worst-off", "three", "worst-off autocallable 3 x 5 dates (contracts/worst-off.cl)"),
     "call": ("european-call", "call", "European call 1 x 1 date (proj/contracts/european-call.cl)"),
@@ -217,7 +225,8 @@ def main():
     kern = E.Kernel(kern_json)
     paths = args.paths_per_gpu * world
     seed = 42
-    literals = batch_literals(kern_json) if args.workload == "brc_batch" else None
+    literals = (batch_literals(kern_json, args.workload) if args.workload.endswith("_batch")
+                else None)
     n_inst = len(literals) if literals else 1
     pricer = DistributedPricer(kern, model_json, [0], device=local, literals=literals, rng=args.rng,
                                jit=args.jit)
@@ -319,9 +328,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and literals is None:
         threads = os.cpu_count() or 1
         kind, dt, r = cpu_reference(kern_json, model_json, args.ref_paths, seed, threads)
+        one = max(1000, args.ref_paths // max(1, threads))
+        _, dt1, _ = cpu_reference(kern_json, model_json, one, seed, 1)
         cpu = {"value": args.ref_paths / dt, "unit": "paths/s", "cores": threads, "kind": kind,
                "sample": f"{args.ref_paths} paths of the same workload, seed {seed}, "
                          f"{dt:.2f} s on {threads} threads",
+               "value_1_thread": one / dt1,
+               "seconds_for_1e9_paths": 1e9 * dt / args.ref_paths,
+               "note": "1e9-path time extrapolated linearly from the sample",
                "price": r["price"], "std_error": r["std_error"]}
 
     if rank == 0:
