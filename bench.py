@@ -36,6 +36,10 @@ F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None
 # brc: ncu r1 (profiles/r1_path_kernel_brc_2M_raw.csv), 2e6 paths:
 #   dadd 6.2471e10 + dmul 7.0817e10 + 2 * dfma 2.19577e11 thread-instructions
 # worst_off / call: first measurement (profiles/r1_fp64ops_*_2M.csv), 2e6 paths
+# QMC mode (Sobol + AS241 + bridge) has its own F_path, frozen from the first
+# measurement (profiles/r1_fp64ops_qmc_brc_2M.csv, 2e6 paths):
+#   dadd 1.61651e10 + dmul 1.73608e10 + 2 * dfma 8.59067e10 thread-instructions
+F_PATH_QMC = {"brc": 102669.7}
 
 BATCH_N = 1024
 
@@ -310,7 +314,7 @@ def main():
     d2h = info["n_outputs"] * 24 + 8
 
     # roofline: FP64 pipe (the kernel reads only constants; no HBM term)
-    fpath = F_PATH.get(args.workload) if args.rng == "philox" else None
+    fpath = F_PATH.get(args.workload) if args.rng == "philox" else F_PATH_QMC.get(args.workload)
     per_gpu_paths = paths / world
     if fpath:
         achieved = per_gpu_paths * n_inst * fpath / (t_kern * 1e-3) / 1e12

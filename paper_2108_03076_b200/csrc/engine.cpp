@@ -74,6 +74,7 @@ struct PlanImpl {
   int blocksPerSm = 0;
   uint32_t nOut = 0;
   const void* jitFn = nullptr;  // NVRTC kernel (cudaKernel_t) or null: interpreter
+  uint64_t drawsPerPath = 0;    // normals per path (chunk sizing)
 
   ~PlanImpl() {
     int cur = 0;
@@ -131,6 +132,8 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   co.rewrite = opt.rewrite;
   I.prog = compileProgram(k, lits, sp, days, co);
   I.nOut = I.prog.header.n_instances * I.prog.header.n_days;
+  for (const cltk_step& st : I.prog.steps)
+    if (st.draws == 1) I.drawsPerPath += I.prog.header.n_assets;
   if (opt.jit < 0 || opt.jit > 2) throw UnsupportedError("unknown jit mode");
   std::string jitSrc;
   if (opt.jit != JIT_OFF) {
@@ -221,6 +224,14 @@ void Plan::chunking(uint64_t paths, uint64_t* chunkPaths, uint64_t* nChunks) con
   uint64_t maxChunks = std::min<uint64_t>(kMaxChunks, kPartialBudget / (sizeof(cltk_partial) * nOut));
   maxChunks = std::max<uint64_t>(1, maxChunks);
   uint64_t ppt = (paths + kBlock * maxChunks - 1) / (kBlock * maxChunks);
+  // Short paths: at least ~64 normal draws per thread per chunk (amortises the
+  // per-chunk scheduling and Chan combine), as long as the run still has
+  // >= 8192 chunks to balance over the grid.  Depends on the program and the
+  // path count only (never on the GPU or its SM count).
+  const uint64_t draws = std::max<uint64_t>(1, impl_->drawsPerPath);
+  const uint64_t pptWork = std::min<uint64_t>(32, (64 + draws - 1) / draws);
+  const uint64_t pptBalance = std::max<uint64_t>(1, paths / (kBlock * 8192ull));
+  ppt = std::max<uint64_t>(ppt, std::min(pptWork, pptBalance));
   ppt = std::max<uint64_t>(1, ppt);
   *chunkPaths = ppt * kBlock;
   *nChunks = (paths + *chunkPaths - 1) / *chunkPaths;
