@@ -190,6 +190,14 @@ SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& model, uint32_t rng) 
     }
     p.steps.push_back(st);
   }
+  const uint32_t nA32 = static_cast<uint32_t>(std::max<std::size_t>(1, n));
+  for (std::size_t s = 0; s < p.steps.size(); ++s) {
+    uint32_t w = 0;
+    for (uint32_t q = 0; (q + 1) * nA32 <= 32 && s + q < p.steps.size(); ++q)
+      if (p.steps[s + q].draws == STEP_DRAW)
+        w |= static_cast<uint32_t>((uint64_t{1} << nA32) - 1) << (q * nA32);
+    p.steps[s].draw_window = w;
+  }
   for (uint32_t a : p.colToAsset) p.usedMask |= 1u << a;
   if (rng == CLTK_RNG_SOBOL) {
     // Same GBM in closed form over the bridge's W(t): logS(t) = log(spot)

@@ -86,6 +86,10 @@ typedef struct {
   // NVRTC mode: the step's op class (steps with identical ops share one;
   // 0 = no ops), the `case` of the generated payoff policy (jit.cpp).
   uint32_t jit_class;
+  // Philox mode: draw-slot mask of the steps s, s+1, ... (bits q*nA .. q*nA+nA-1
+  // set when step s+q draws; q < 32 / nA): a normal batch starting at step s
+  // masks it to its own slots (domain errors count only for drawn indices).
+  uint32_t draw_window;
 } cltk_step;
 
 // Brownian-bridge construction op (QMC mode): for every asset j
