@@ -288,6 +288,8 @@ def main():
     # end to end through the public API, host JSON in -> host results out; one
     # untimed call first (process-level caches: CUDA context, NVRTC module)
     e2e_times = []
+    clocks_e2e = ClockSampler(local)
+    clocks_e2e.start()
     for it in range(args.e2e_steps + (1 if args.e2e_steps else 0)):
         barrier()
         t0 = time.perf_counter()
@@ -303,6 +305,7 @@ def main():
         torch.cuda.synchronize(dev)
         if it:
             e2e_times.append(time.perf_counter() - t0)
+    clk_e2e = clocks_e2e.stop()
     t_e2e = sum(e2e_times) / max(1, len(e2e_times))
     if world > 1:
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
@@ -360,7 +363,7 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": paths * n_inst / t_e2e if t_e2e > 0 else None, "unit": "paths/s",
                         "h2d_bytes_per_step": h2d, "samples_ms": [round(t * 1e3, 3) for t in e2e_times],
-                        "d2h_bytes_per_step": d2h,
+                        "d2h_bytes_per_step": d2h, "clocks": clk_e2e,
                         "path": "paper_2108_03076_b200.price -> cltk_gpu_price[_ex] (C-ABI), host "
                                 "kernel/model JSON in, host results out"},
                 "gpu_launches": 2, "clocks": clk,
