@@ -251,6 +251,7 @@ def main():
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(1.5)  # nvidia-smi start-up (NVML init) outside the timed steps
     step_ms = []
     kernel_ms = []
     res = None
@@ -290,6 +291,7 @@ def main():
     e2e_times = []
     clocks_e2e = ClockSampler(local)
     clocks_e2e.start()
+    time.sleep(1.5)  # nvidia-smi start-up (NVML init) outside the timed calls
     for it in range(args.e2e_steps + (1 if args.e2e_steps else 0)):
         barrier()
         t0 = time.perf_counter()

@@ -501,9 +501,13 @@ def debug_math(fn: str, x, device: int = -1):
     the reference's ``inv_normal`` (invNormalCdf) over an array; ``div``
     (pairs ``x[2i] / x[2i+1]`` through the engine's bounded-range division,
     written to both slots) and ``halley_arg`` (``-x / sqrt(2.0)``) check the
-    engine's division shortcuts against IEEE."""
+    engine's division shortcuts against IEEE; ``log_fmin`` / ``log_fmax``
+    (pairs ``(m, x)``: ``exp`` of the running minimum / maximum the NVRTC
+    payoff code keeps in the log domain, both slots) against
+    ``fmin(exp(m), exp(x))`` / ``fmax``."""
     import numpy as np
-    code = {"exp": 0, "log": 1, "erfc": 2, "inv_normal": 3, "div": 4, "halley_arg": 5}[fn]
+    code = {"exp": 0, "log": 1, "erfc": 2, "inv_normal": 3, "div": 4, "halley_arg": 5,
+            "log_fmin": 6, "log_fmax": 7}[fn]
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.zeros_like(x)
     err = _native.ErrorC()

@@ -236,31 +236,64 @@ struct Gen {
     }
   }
 
+  // Log-domain spots (logMode, engine_device.cuh: spot_exp / log_fmin): a
+  // step receives the logarithms L[j] of its spots; S[j] = exp(L[j]) is
+  // formed only where an op needs the spot itself, and running minima /
+  // maxima of spots (fmin / fmax of two log-capable operands: a slot or a
+  // log-domain value) stay logarithms, exponentiated once where something
+  // else reads them.  A thread register carries a log-domain value across
+  // steps when every step-class occurrence sees it in the same domain
+  // (entryDom, found by simulating the step sequence in jitSource); noLog
+  // registers are always stored as values.
+  bool logMode = false;
+  std::set<uint32_t> noLog;
+  std::map<uint32_t, std::map<uint32_t, int>> entryDom;  // class -> register -> 1 if log
+
+  struct Val {
+    std::string log, val;  // log form (log-domain value) and/or value form
+  };
+
   // Straight-line emission of one block with its values in locals: a register
   // is loaded from its shared-memory column at its first read in the block (if
   // not yet written there), every op result is a new local, and at the end a
   // register is stored back only if something outside the block can read it
   // (another block, the outputs, or this block's next occurrence -- a read
-  // before the write).  Same ops, same order, same IEEE operations.
-  void emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep, uint32_t block,
-            const char* ind) const {
-    std::map<uint32_t, std::string> cur;
+  // before the write).  Same ops, same order, same IEEE operations (log-domain
+  // minima / maxima: bitwise the same results).  Returns the domain (1: log)
+  // of every register written in the block.
+  std::map<uint32_t, int> emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep,
+                               uint32_t block, const char* ind) const {
+    std::map<uint32_t, Val> cur;
+    std::map<uint32_t, Val> slotVal;  // materialised spots of this block
     std::set<uint32_t> dirty, carried;
     int n = 0;
+    const bool lm = logMode && inStep && sRegs;
+    const auto ent = entryDom.find(block);
     if (inStep && !sRegs)
       for (uint32_t j = 0; j < nA; ++j) {
-        cur[j] = "S[" + std::to_string(j) + "]";
+        cur[j] = Val{"", "S[" + std::to_string(j) + "]"};
         dirty.insert(j);
       }
-    auto val = [&](uint32_t i) -> std::string {
-      if (i < nA && inStep && sRegs) return "S[" + std::to_string(i) + "]";
+    auto fresh = [&]() { return "v" + std::to_string(n++); };
+    auto operand = [&](uint32_t i) -> Val {
+      if (i < nA && inStep && sRegs) {
+        if (!lm) return Val{"", "S[" + std::to_string(i) + "]"};
+        auto it = slotVal.find(i);
+        if (it != slotVal.end()) return it->second;
+        return slotVal[i] = Val{"L[" + std::to_string(i) + "]", ""};
+      }
       auto it = cur.find(i);
       if (it != cur.end()) return it->second;
-      const std::string v = "v" + std::to_string(n++);
+      const std::string v = fresh();
       std::string src;
+      bool isLog = false;
       if (i < nThread) {
         carried.insert(i);
         src = "JR(" + std::to_string(i) + ")";
+        if (ent != entryDom.end()) {
+          auto e = ent->second.find(i);
+          isLog = e != ent->second.end() && e->second;
+        }
       } else if (!copyInst && i >= nThread + nc && i < nThread + nc + ni) {
         // instance literals straight from the table (L1-resident, broadcast)
         src = "JI(" + std::to_string(i - nThread - nc) + ")";
@@ -268,30 +301,74 @@ struct Gen {
         src = "JC(" + std::to_string(i) + ")";
       }
       os << ind << "const double " << v << " = " << src << ";\n";
-      cur[i] = v;
+      return cur[i] = isLog ? Val{v, ""} : Val{"", v};
+    };
+    // the value form of operand i (exp of a log-domain value, formed once)
+    auto value = [&](uint32_t i) -> std::string {
+      Val x = operand(i);
+      if (!x.val.empty()) return x.val;
+      const std::string v = fresh();
+      os << ind << "const double " << v << " = spot_exp(" << x.log << ");\n";
+      x.val = v;
+      if (i < nA && inStep && sRegs) slotVal[i] = x;
+      else cur[i] = x;
       return v;
     };
     for (const DOp& o : ops) {
       if (o.op == OP_NOP) continue;
-      const std::string a = val(o.a);
-      const std::string b = usesB(o.op) ? val(o.b) : std::string();
-      const std::string c = o.op == OP_SEL ? val(o.c) : std::string();
-      const std::string t = "v" + std::to_string(n++);
-      os << ind << "double " << t << ";\n" << ind << "{ const double a = " << a << ";";
-      if (!b.empty()) os << " const double b = " << b << ";";
-      if (!c.empty()) os << " const double c = " << c << ";";
-      os << " " << t << " = " << opExpr(o) << "; }\n";
-      cur[o.d] = t;
+      Val res;
+      const std::string t = o.op == OP_MOV ? std::string() : fresh();
+      if (o.op == OP_MOV) {
+        res = operand(o.a);  // a copy: the same local(s)
+      } else if (lm && (o.op == OP_MIN || o.op == OP_MAX) && !operand(o.a).log.empty() &&
+                 !operand(o.b).log.empty()) {
+        const std::string a = operand(o.a).log, b = operand(o.b).log;
+        os << ind << "const double " << t << " = " << (o.op == OP_MIN ? "log_fmin(" : "log_fmax(")
+           << a << ", " << b << ");\n";
+        res = Val{t, ""};
+      } else {
+        const std::string a = value(o.a);
+        const std::string b = usesB(o.op) ? value(o.b) : std::string();
+        const std::string c = o.op == OP_SEL ? value(o.c) : std::string();
+        os << ind << "double " << t << ";\n" << ind << "{ const double a = " << a << ";";
+        if (!b.empty()) os << " const double b = " << b << ";";
+        if (!c.empty()) os << " const double c = " << c << ";";
+        os << " " << t << " = " << opExpr(o) << "; }\n";
+        res = Val{"", t};
+      }
+      cur[o.d] = res;
+      if (!res.log.empty() && noLog.count(o.d)) value(o.d);  // stored as a value
       dirty.insert(o.d);
     }
+    std::map<uint32_t, int> exitDom;
     for (uint32_t r : dirty) {
+      const Val& x = cur[r];
+      const bool isLog = x.val.empty();
+      exitDom[r] = isLog ? 1 : 0;
       bool live = outRead.count(r) || carried.count(r);
       auto it = readBy.find(r);
       if (!live && it != readBy.end())
         for (uint32_t bl : it->second)
           if (bl != block) live = true;
-      if (live) os << ind << "JW(" << r << ", " << cur[r] << ");\n";
+      if (live) os << ind << "JW(" << r << ", " << (isLog ? x.log : x.val) << ");\n";
     }
+    return exitDom;
+  }
+
+  // Registers a block reads before writing them (its entry state).
+  static std::set<uint32_t> readsFirst(const std::vector<DOp>& ops, uint32_t nThread) {
+    std::set<uint32_t> w, r;
+    auto rd = [&](uint32_t i) {
+      if (i < nThread && !w.count(i)) r.insert(i);
+    };
+    for (const DOp& o : ops) {
+      if (o.op == OP_NOP) continue;
+      rd(o.a);
+      if (usesB(o.op)) rd(o.b);
+      if (o.op == OP_SEL) rd(o.c);
+      w.insert(o.d);
+    }
+    return r;
   }
 };
 
@@ -369,6 +446,46 @@ std::string jitSource(CompiledProgram& prog) {
     if (o.val < h.n_thread) g.outRead.insert(o.val);
     if (o.err != CLTK_NO_ERR && o.err < h.n_thread) g.outRead.insert(o.err);
   }
+  // Log-domain spots: find each step class's entry domains by running the
+  // step sequence; a register seen in two domains at one class's entry, or
+  // still log-domain when the outputs / the instance section read it, is
+  // stored as a value everywhere (noLog) and the sequence is re-run.
+  g.logMode = g.sRegs && std::getenv("CLTK_JIT_NO_LOGSPOTS") == nullptr;
+  if (g.logMode) {
+    std::vector<std::set<uint32_t>> firstReads(classOps.size());
+    for (size_t c = 1; c < classOps.size(); ++c)
+      firstReads[c] = Gen::readsFirst(classOps[c], h.n_thread);
+    std::set<uint32_t> endReads(g.outRead);
+    for (uint32_t r : Gen::readsFirst(instOps, h.n_thread)) endReads.insert(r);
+    for (;;) {
+      g.entryDom.clear();
+      std::map<uint32_t, std::map<uint32_t, int>> exitDom;  // per class, fixed entries
+      std::map<uint32_t, int> dom;
+      uint32_t bad = ~0u;
+      for (const cltk_step& st : prog.steps) {
+        const uint32_t c = st.jit_class;
+        if (c == 0) continue;
+        const bool first = !g.entryDom.count(c);
+        std::map<uint32_t, int>& ent = g.entryDom[c];
+        for (uint32_t r : firstReads[c]) {
+          const int d = dom.count(r) ? dom[r] : 0;
+          if (first) ent[r] = d;
+          else if (ent[r] != d) bad = r;
+        }
+        if (bad != ~0u) break;
+        if (first) {
+          std::ostringstream dry;
+          exitDom[c] = g.emit(dry, classOps[c], true, c, "");
+        }
+        for (const auto& kv : exitDom[c]) dom[kv.first] = kv.second;
+      }
+      if (bad == ~0u)
+        for (uint32_t r : endReads)
+          if (dom.count(r) && dom[r]) bad = r;
+      if (bad == ~0u) break;
+      g.noLog.insert(bad);
+    }
+  }
   std::ostringstream os;
   os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
         "#define CLTK_JIT 1\n"
@@ -386,9 +503,12 @@ std::string jitSource(CompiledProgram& prog) {
         "struct JitPayoff {\n"
         "  static constexpr bool kCopyInstConst = "
      << (g.copyInst ? "true" : "false") << ";\n"
+        "  static constexpr bool kLogSpots = "
+     << (g.logMode ? "true" : "false") << ";\n"
         "  template <int NA>\n"
         "  static __device__ __forceinline__ void step(const Frame f, const DevPlan& P,\n"
-        "                                              const cltk_step* st, const double (&S)[NA]) {\n"
+        "                                              const cltk_step* st, const double (&"
+     << (g.logMode ? "L" : "S") << ")[NA]) {\n"
         "    switch (__ldg(&st->jit_class)) {\n";
   for (size_t c = 1; c < classOps.size(); ++c) {
     os << "      case " << c << ": {\n";

@@ -48,7 +48,8 @@ def test_brc_source_structure():
     src = E.jit_source(k, m, [0])
     cases = re.findall(r"case (\d+): \{", src)
     assert len(cases) == 3, cases
-    assert "S[0]" in src and "fmin(a, b)" in src
+    # spots arrive as logarithms; the running minima stay in the log domain
+    assert "kLogSpots = true" in src and "L[0]" in src and "log_fmin(" in src
     for lit in ("2630.635", "8288", "840"):
         assert lit not in src
     # a different literal instance of the template: identical source
@@ -132,3 +133,44 @@ def test_jit_division_by_zero_raises_like_interpreter():
                      "then": kern["body"], "else": {"kind": "float", "value": 2.0}},
             "rows": [5], "cols": ["AAPL"], "tvars": [], "parties": [], "horizon": 6}
     assert E.price(E.Kernel(safe), load_model("call"), 1000, 1, jit=True)[0]["price"] == 2.0
+
+
+def _up_barrier_brc():
+    """The BRC with its knock-in turned into an up-and-in at 130% of spot
+    (literal on the left of <=): the OR chains become running maxima."""
+    k = load_kernel("brc")
+    up = {2630.635: 3758.05 * 1.3, 8288.0: 11840.0 * 1.3, 840.0: 1200.0 * 1.3}
+
+    def walk(e):
+        if isinstance(e, dict):
+            if (e.get("kind") == "binop" and e.get("op") == "leq" and
+                    e["left"].get("kind") == "obsref" and e["right"].get("kind") == "float" and
+                    e["right"]["value"] in up):
+                return {"kind": "binop", "op": "leq",
+                        "left": {"kind": "float", "value": up[e["right"]["value"]]},
+                        "right": e["left"]}
+            return {kk: walk(v) for kk, v in e.items()}
+        if isinstance(e, list):
+            return [walk(v) for v in e]
+        return e
+    return walk(k)
+
+
+def test_up_barrier_source_uses_log_fmax():
+    src = E.jit_source(E.Kernel(_up_barrier_brc()), load_model("three"), [0, 100])
+    assert "log_fmax(" in src and "kLogSpots = true" in src
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["down", "up"])
+def test_log_domain_extrema_bitwise_vs_interpreter(variant):
+    """Log-domain running minima (BRC knock-in) and maxima (up-and-in
+    variant): NVRTC prices equal the interpreter's bit for bit, several
+    valuation days, both RNG modes."""
+    k = E.Kernel(load_kernel("brc") if variant == "down" else _up_barrier_brc())
+    m = load_model("three")
+    for rng in ("philox", "sobol"):
+        a = E.price(k, m, 40000, 7, [0, 100, 300], rng=rng, jit=False)
+        b = E.price(k, m, 40000, 7, [0, 100, 300], rng=rng, jit=True)
+        for x, y in zip(a, b):
+            assert x["price"] == y["price"] and x["std_error"] == y["std_error"], (rng, x, y)
