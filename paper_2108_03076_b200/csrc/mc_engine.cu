@@ -30,7 +30,7 @@ cudaError_t launchPathT(const DevPlan& p, const RunArgs& a, int grid, size_t sme
 size_t bridgeWords(const cltk_plan_header& h) {
   if (h.rng != CLTK_RNG_SOBOL) return 0;
   const size_t need = static_cast<size_t>(h.n_bridge_slots) * (h.n_assets ? h.n_assets : 1) * kBlock;
-  const size_t have = kMaxBatch * kBlock;  // the Y slots
+  const size_t have = static_cast<size_t>(batchSlots(h.n_assets ? h.n_assets : 1)) * kBlock;  // the Y slots
   return need > have ? need - have : 0;
 }
 
@@ -38,7 +38,8 @@ template <int NA, bool QMC>
 cudaError_t launchDumpT(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
   const cltk_plan_header& h = p.hdr;
   size_t smem = (static_cast<size_t>(h.n_thread) * kBlock +
-                 kWarps * (h.n_shared_const + h.n_inst_const) + kNormScratchWords + bridgeWords(h)) *
+                 kWarps * (h.n_shared_const + h.n_inst_const) + normScratchWords(h.n_assets ? h.n_assets : 1) +
+                 bridgeWords(h)) *
                 sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(dump_kernel<NA, QMC>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -69,7 +70,7 @@ size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
                  kWarps * (h.n_shared_const + h.n_inst_const);
   if (accInSmem) words += kWarps * nOut * 3;
   words += kWarps + 1;  // counts + chunk slot
-  words += kNormScratchWords;
+  words += normScratchWords(h.n_assets ? h.n_assets : 1);
   words += bridgeWords(h);
   return words * sizeof(double);
 }
