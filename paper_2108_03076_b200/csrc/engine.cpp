@@ -6,8 +6,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 
 #include "cltk_b200.hpp"
@@ -24,11 +28,38 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Plan buffers come from the device's stream-ordered pool with an unbounded
+// release threshold: a one-shot call's frees return memory to the pool
+// instead of unmapping it (cudaFree stalled single calls by 50-500 ms).
+void* devMalloc(size_t bytes) {
+  static std::mutex mu;
+  static bool configured[64] = {};
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && !configured[dev]) {
+      cudaMemPool_t pool;
+      ck(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
+      uint64_t keep = ~0ULL;
+      ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep),
+         "cudaMemPoolSetAttribute");
+      configured[dev] = true;
+    }
+  }
+  void* p = nullptr;
+  ck(cudaMallocAsync(&p, bytes, 0), "cudaMallocAsync");
+  ck(cudaStreamSynchronize(0), "cudaStreamSynchronize");  // usable from any stream
+  return p;
+}
+void devFree(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+
 template <class T>
 T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
   if (v.empty()) return nullptr;
-  void* p = nullptr;
-  ck(cudaMalloc(&p, v.size() * sizeof(T)), "cudaMalloc");
+  void* p = devMalloc(v.size() * sizeof(T));
   ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
   owned.push_back(p);
   return static_cast<T*>(p);
@@ -80,9 +111,10 @@ struct PlanImpl {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
-    for (void* p : owned) cudaFree(p);
-    if (accScratch) cudaFree(accScratch);
-    if (ownPartials) cudaFree(ownPartials);
+    cudaDeviceSynchronize();  // no launch of this plan may still be reading its buffers
+    for (void* p : owned) devFree(p);
+    devFree(accScratch);
+    devFree(ownPartials);
     cudaSetDevice(cur);
   }
 
@@ -169,12 +201,12 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
     I.dev.sobolT5 = upload(T5, I.owned);
   }
   void* p = nullptr;
-  ck(cudaMalloc(&p, 2 * sizeof(unsigned long long)), "cudaMalloc");
+  p = devMalloc(2 * sizeof(unsigned long long));
   I.owned.push_back(p);
   I.errKey = static_cast<unsigned long long*>(p);
   I.chunkCounter = I.errKey + 1;
   ck(cudaMemset(I.errKey, 0xff, sizeof(unsigned long long)), "cudaMemset");
-  ck(cudaMalloc(&p, std::max<size_t>(1, I.nOut) * sizeof(cltk_partial)), "cudaMalloc");
+  p = devMalloc(std::max<size_t>(1, I.nOut) * sizeof(cltk_partial));
   I.owned.push_back(p);
   I.combined = static_cast<cltk_partial*>(p);
   I.accInSmem = accFitsSmem(I.prog.header);
@@ -244,7 +276,7 @@ const uint32_t* sobolShiftFor(PlanImpl& I, uint64_t seed, cudaStream_t s) {
   if (I.prog.header.rng != CLTK_RNG_SOBOL || seed == 0) return nullptr;
   if (!I.sobolShift) {
     void* p = nullptr;
-    ck(cudaMalloc(&p, kSobolDims * sizeof(uint32_t)), "cudaMalloc");
+    p = devMalloc(kSobolDims * sizeof(uint32_t));
     I.owned.push_back(p);
     I.sobolShift = static_cast<uint32_t*>(p);
     I.shiftSeed = seed + 1;  // force the first upload
@@ -279,8 +311,9 @@ void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void*
   if (!I.accInSmem) {
     size_t need = static_cast<size_t>(grid);
     if (need > I.accScratchBlocks) {
-      if (I.accScratch) cudaFree(I.accScratch);
-      ck(cudaMalloc(&I.accScratch, need * kWarps * I.nOut * 3 * sizeof(double)), "cudaMalloc");
+      ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+      devFree(I.accScratch);
+      I.accScratch = static_cast<double*>(devMalloc(need * kWarps * I.nOut * 3 * sizeof(double)));
       I.accScratchBlocks = need;
     }
   }
@@ -473,9 +506,9 @@ std::vector<PriceResult> runOnce(Plan& plan, uint64_t paths, uint64_t seed,
   uint64_t chunkPaths, nChunks;
   plan.chunking(paths, &chunkPaths, &nChunks);
   if (nChunks > I.ownPartialsChunks) {
-    if (I.ownPartials) cudaFree(I.ownPartials);
-    ck(cudaMalloc(&I.ownPartials, nChunks * std::max<uint32_t>(1, I.nOut) * sizeof(cltk_partial)),
-       "cudaMalloc partials");
+    devFree(I.ownPartials);
+    I.ownPartials = static_cast<cltk_partial*>(
+        devMalloc(nChunks * std::max<uint32_t>(1, I.nOut) * sizeof(cltk_partial)));
     I.ownPartialsChunks = nChunks;
   }
   cudaStream_t s = nullptr;
@@ -496,14 +529,41 @@ std::vector<PriceResult> runOnce(Plan& plan, uint64_t paths, uint64_t seed,
 
 }  // namespace
 
+namespace {
+// A one-shot call: plan, run on its own buffers, free.  CLTK_TRACE=1 prints
+// where the host time goes (stderr).
+template <class MakePlan>
+std::vector<PriceResult> oneShot(MakePlan make, uint64_t paths, uint64_t seed,
+                                 const std::vector<uint64_t>& days) {
+  static const bool trace = std::getenv("CLTK_TRACE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  std::vector<PriceResult> r;
+  double tPlan = 0.0, tRun = 0.0;
+  {
+    std::unique_ptr<Plan> plan = make();
+    if (days.empty()) return {};
+    const auto t1 = clk::now();
+    r = runOnce(*plan, paths, seed, days);
+    tPlan = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    tRun = std::chrono::duration<double, std::milli>(clk::now() - t1).count();
+  }
+  if (trace) {
+    const double tAll = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    std::fprintf(stderr, "[cltk] one-shot price: plan %.2f ms, run %.2f ms, free %.2f ms\n",
+                 tPlan, tRun, tAll - tPlan - tRun);
+  }
+  return r;
+}
+}  // namespace
+
 std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,
                                     const ModelSpec& model, uint64_t paths, uint64_t seed,
                                     const std::vector<uint64_t>& days, const TEnv& tenv,
                                     const RunOptions& opt) {
   if (paths == 0) throw EvalError("path count must be positive");
-  Plan plan(instances, model, days, tenv, opt);
-  if (days.empty()) return {};
-  return runOnce(plan, paths, seed, days);
+  return oneShot([&] { return std::make_unique<Plan>(instances, model, days, tenv, opt); }, paths,
+                 seed, days);
 }
 
 std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* literals,
@@ -512,9 +572,11 @@ std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* litera
                                        const std::vector<uint64_t>& days, const TEnv& tenv,
                                        const RunOptions& opt) {
   if (paths == 0) throw EvalError("path count must be positive");
-  Plan plan(templ, literals, nInstances, nLits, model, days, tenv, opt);
-  if (days.empty()) return {};
-  return runOnce(plan, paths, seed, days);
+  return oneShot(
+      [&] {
+        return std::make_unique<Plan>(templ, literals, nInstances, nLits, model, days, tenv, opt);
+      },
+      paths, seed, days);
 }
 
 std::vector<PriceResult> priceAcrossTime(const Kernel& k, const ModelSpec& model,
