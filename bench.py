@@ -41,6 +41,14 @@ F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None
 #   dadd 1.61651e10 + dmul 1.73608e10 + 2 * dfma 8.59067e10 thread-instructions
 F_PATH_QMC = {"brc": 102669.7}
 
+# DRAM bytes per launch of the path kernel from the committed ncu --set full
+# capture (dram__bytes_read.sum + dram__bytes_write.sum; the kernel reads only
+# its ~90 KB program and the partials stay in L2), and the FP64 pipe activity
+# ncu measured there -- the kernel's own pipe utilisation beside the frozen-F
+# roofline fraction.
+NCU_EVIDENCE = {"brc": {"traffic": 206848.0, "fp64_pipe_active": 0.488,
+                        "capture": "profiles/r1j_path_kernel_brc_10M_raw.csv (10M-path launch)"}}
+
 BATCH_N = 1024
 
 
@@ -324,10 +332,14 @@ def main():
     per_gpu_paths = paths / world
     if fpath:
         achieved = per_gpu_paths * n_inst * fpath / (t_kern * 1e-3) / 1e12
+        ev = NCU_EVIDENCE.get(args.workload) if args.rng == "philox" and n_inst == 1 else None
         roof = {"bound": "fp64", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
-                "frac": achieved / peak_tflops, "traffic": None,
+                "frac": achieved / peak_tflops, "traffic": ev["traffic"] if ev else None,
                 "peak_source": "measured DFMA microbenchmark (cltk_fp64_peak), this GPU, burst",
                 "f_path": fpath}
+        if ev:
+            roof.update({"traffic_unit": "bytes per launch", "ncu_capture": ev["capture"],
+                         "fp64_pipe_active_ncu": ev["fp64_pipe_active"]})
     else:
         roof = {"bound": "fp64", "achieved": None, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": None, "traffic": None,
