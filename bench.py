@@ -322,6 +322,10 @@ def main():
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt[0])
+    # our kernels per timed step: the path kernel + the fixed-order combine
+    # (two launches when the chunk count is split, engine_launch.hpp kCombineSplit)
+    n_chunks = pricer.plan.chunking(paths)[1]
+    n_launches = 1 + (2 if (n_chunks + 4095) // 4096 > 1 else 1)
     L = pricer.plan.dump()
     h2d = (len(L["ops"]) * 8 + len(L["steps"]) * 224 + (L["n_shared_const"] + L["n_inst_const"]) * 8
            + len(L["outputs"]) * 8 + 16 + len(kern_json) * 0)
@@ -382,7 +386,7 @@ def main():
                         "d2h_bytes_per_step": d2h, "clocks": clk_e2e,
                         "path": "paper_2108_03076_b200.price -> cltk_gpu_price[_ex] (C-ABI), host "
                                 "kernel/model JSON in, host results out"},
-                "gpu_launches": 2, "clocks": clk,
+                "gpu_launches": n_launches, "clocks": clk,
                 "price": res[0]["price"], "std_error": res[0]["std_error"],
                 "plan": {k: info[k] for k in ("n_shared_ops", "n_thread", "dag_nodes", "jit")}}
         print(json.dumps(line), flush=True)

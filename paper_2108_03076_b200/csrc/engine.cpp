@@ -206,7 +206,8 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   I.errKey = static_cast<unsigned long long*>(p);
   I.chunkCounter = I.errKey + 1;
   ck(cudaMemset(I.errKey, 0xff, sizeof(unsigned long long)), "cudaMemset");
-  p = devMalloc(std::max<size_t>(1, I.nOut) * sizeof(cltk_partial));
+  // [n_out] results, then the [kCombineSplit][n_out] combine intermediates
+  p = devMalloc((1 + kCombineSplit) * std::max<size_t>(1, I.nOut) * sizeof(cltk_partial));
   I.owned.push_back(p);
   I.combined = static_cast<cltk_partial*>(p);
   I.accInSmem = accFitsSmem(I.prog.header);
@@ -351,7 +352,8 @@ std::vector<PriceResult> Plan::finalize(uint64_t paths, uint64_t seed, const voi
   std::vector<cltk_partial> host(I.nOut);
   unsigned long long key = ~0ULL;
   if (I.nOut) {
-    ck(launchCombine(static_cast<const cltk_partial*>(partialsDev), nChunks, I.nOut, I.combined, s),
+    ck(launchCombine(static_cast<const cltk_partial*>(partialsDev), nChunks, I.nOut,
+                     I.combined + std::max<uint32_t>(1, I.nOut), I.combined, s),
        "combine launch");
     ck(cudaMemcpyAsync(host.data(), I.combined, I.nOut * sizeof(cltk_partial),
                        cudaMemcpyDeviceToHost, s),

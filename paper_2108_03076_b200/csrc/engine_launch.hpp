@@ -14,8 +14,11 @@ bool accFitsSmem(const cltk_plan_header& h);
 int pathKernelOccupancy(const cltk_plan_header& h, size_t smem);
 cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
                        cudaStream_t s);
+// Chunk partials -> one (n, mean, M2) per output.  Large chunk counts go
+// through kCombineSplit-wide intermediates (scratch: kCombineSplit * nOut).
+constexpr uint32_t kCombineSplit = 64;
 cudaError_t launchCombine(const cltk_partial* parts, uint64_t nChunks, uint32_t nOut,
-                          cltk_partial* out, cudaStream_t s);
+                          cltk_partial* scratch, cltk_partial* out, cudaStream_t s);
 cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s);
 cudaError_t launchRngDump(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
                           uint64_t* bits, double* uniform, double* normal, cudaStream_t s);

@@ -109,9 +109,20 @@ cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
   CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return (launchDumpT<NA, false>(p, a, s)));
 }
 
+uint32_t combineSplit(uint64_t nChunks) {
+  const uint64_t g = (nChunks + 4095) / 4096;  // >= 16 chunks per thread
+  return static_cast<uint32_t>(g < 1 ? 1 : (g > kCombineSplit ? kCombineSplit : g));
+}
+
 cudaError_t launchCombine(const cltk_partial* parts, uint64_t nChunks, uint32_t nOut,
-                          cltk_partial* out, cudaStream_t s) {
-  combine_kernel<<<nOut, 256, 0, s>>>(parts, nChunks, nOut, out);
+                          cltk_partial* scratch, cltk_partial* out, cudaStream_t s) {
+  const uint32_t g = combineSplit(nChunks);
+  if (g == 1) {
+    combine_kernel<<<dim3(nOut, 1), 256, 0, s>>>(parts, nChunks, nOut, out);
+    return cudaGetLastError();
+  }
+  combine_kernel<<<dim3(nOut, g), 256, 0, s>>>(parts, nChunks, nOut, scratch);
+  combine_kernel<<<dim3(nOut, 1), 256, 0, s>>>(scratch, g, nOut, out);
   return cudaGetLastError();
 }
 
