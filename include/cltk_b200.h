@@ -115,6 +115,14 @@ int cltk_gpu_price_template(const char* kernel_json, const double* literals, siz
                             uint64_t seed, const uint64_t* days, size_t n_days,
                             const char* tenv_json, int device, cltk_price_result* results,
                             cltk_error* err);
+/* Host-only: reindex (proj/src/kernel.cpp:301-303, KernelBuilder :14-180) --
+ * the IL of a compiled contract in its JSON wire format (ilToJson,
+ * proj/src/json_io.cpp:203-255) flattened into the kernel JSON
+ * (kernelToJson, proj/src/kernel.cpp:620) every pricing entry point takes,
+ * template variables bound from tenv_json.  Malloc'd; free with cltk_free.
+ * Errors: ParseError for malformed IL, EvalError for an unbound template
+ * variable (proj/include/cltk/errors.hpp:51-54). */
+int cltk_reindex(const char* il_json, const char* tenv_json, char** kernel_json, cltk_error* err);
 /* Host-only: the kernel's float literals in the order above (*n = count;
  * at most cap values written). */
 int cltk_kernel_literals(const char* kernel_json, double* out, size_t cap, size_t* n,

@@ -266,6 +266,10 @@ class Ref:
         L.cltkref_free.argtypes = [vp]
         L.cltkref_compile_kernel_json.restype = i32
         L.cltkref_compile_kernel_json.argtypes = [C.c_char_p, C.c_char_p, i32, C.POINTER(vp)]
+        L.cltkref_compile_il_json.restype = i32
+        L.cltkref_compile_il_json.argtypes = [C.c_char_p, i32, C.POINTER(vp)]
+        L.cltkref_reindex_json.restype = i32
+        L.cltkref_reindex_json.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(vp)]
         L.cltkref_kernel_source.restype = i32
         L.cltkref_kernel_source.argtypes = [C.c_char_p, C.POINTER(vp)]
         L.cltkref_philox_bits.restype = u64
@@ -314,6 +318,18 @@ class Ref:
         out = C.c_void_p()
         self._check(self.lib.cltkref_compile_kernel_json(
             contract_src.encode(), json.dumps(tenv or {}).encode(), int(cut), C.byref(out)))
+        return json.loads(self._take_string(out))
+
+    def compile_il(self, contract_src: str, cut: bool = True) -> dict:
+        """ilToJson(cutPayoff?(compileContract(parse(src)))) -- reindex's input."""
+        out = C.c_void_p()
+        self._check(self.lib.cltkref_compile_il_json(contract_src.encode(), int(cut), C.byref(out)))
+        return json.loads(self._take_string(out))
+
+    def reindex(self, il: dict, tenv: dict | None = None) -> dict:
+        out = C.c_void_p()
+        self._check(self.lib.cltkref_reindex_json(json.dumps(il).encode(),
+                                                  json.dumps(tenv or {}).encode(), C.byref(out)))
         return json.loads(self._take_string(out))
 
     def kernel_source(self, kernel: dict) -> str:

@@ -102,6 +102,26 @@ int cltkref_compile_kernel_json(const char* src, const char* tenvJson, int cut,
   });
 }
 
+// The IL the reference hands to reindex (ilToJson, proj/src/json_io.cpp:203),
+// optionally after cutPayoff -- fixtures for the engine's own reindex.
+int cltkref_compile_il_json(const char* src, int cut, char** out) {
+  return guarded([&] {
+    ContrPtr c = parseContract(src);
+    typeCheckContr(TypeCtx{}, c);
+    ILPtr il = compileContract(c);
+    if (cut) il = cutPayoff(il);
+    *out = dupString(ilToJson(il).dump());
+  });
+}
+
+// reindex (proj/src/kernel.cpp:301-303) of an IL in its JSON wire format.
+int cltkref_reindex_json(const char* ilJson, const char* tenvJson, char** out) {
+  return guarded([&] {
+    Kernel k = reindex(ilFromJson(nlohmann::json::parse(ilJson)), tenvOf(tenvJson));
+    *out = dupString(kernelToJson(k).dump());
+  });
+}
+
 int cltkref_kernel_source(const char* kernelJson, char** out) {
   return guarded([&] {
     Kernel k = kernelFromJson(nlohmann::json::parse(kernelJson));

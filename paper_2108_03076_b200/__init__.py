@@ -36,7 +36,7 @@ __all__ = [
     "Kernel", "ContractError", "ContractParseError", "ContractTypeError",
     "ContractUnsupportedError", "price", "price_batch", "black_scholes_call", "Plan",
     "compile_listing", "debug_rng", "debug_math", "fp64_peak", "load_kernel", "version",
-    "kernel_literals", "price_template", "jit_source", "jit_compile",
+    "kernel_literals", "price_template", "jit_source", "jit_compile", "reindex",
 ]
 
 
@@ -334,6 +334,20 @@ def compile_listing(kernels: Sequence[Kernel | str | dict] | Kernel, model: str 
     s = C.cast(out, C.c_char_p).value.decode()
     L.cltk_free(out)
     return _deep(json.loads, s)
+
+
+def reindex(il: str | dict, tenv: dict | None = None) -> Kernel:
+    """reindex (proj/src/kernel.cpp:301-303): the IL of a compiled contract
+    (its JSON wire format, ``ilToJson``) flattened into a pricing kernel, the
+    template variables bound from ``tenv``.  Host only."""
+    L = _native.lib()
+    ij = (il if isinstance(il, str) else json.dumps(il)).encode()
+    out = C.c_void_p()
+    err = _native.ErrorC()
+    _raise(L.cltk_reindex(ij, _tenv_json(tenv), C.byref(out), C.byref(err)), err)
+    s = C.cast(out, C.c_char_p).value.decode()
+    L.cltk_free(out)
+    return Kernel(s)
 
 
 def jit_source(kernel: Kernel | str | dict, model: str | dict, days: Sequence[int] = (0,),

@@ -20,7 +20,7 @@ EXPORTS = [
     "cltk_compile_listing", "cltk_plan_dump", "cltk_free", "cltk_debug_paths", "cltk_debug_rng", "cltk_debug_math",
     "cltk_fp64_peak", "cltk_black_scholes_call", "cltk_gpu_price_template",
     "cltk_kernel_literals", "cltk_plan_create_template", "cltk_gpu_price_ex",
-    "cltk_plan_create_ex", "cltk_jit_source", "cltk_jit_compile",
+    "cltk_plan_create_ex", "cltk_jit_source", "cltk_jit_compile", "cltk_reindex",
     "cltk_plan_create_batch_ex", "cltk_gpu_price_batch_ex",
 ]
 
@@ -103,6 +103,8 @@ def lib() -> C.CDLL:
     L.cltk_plan_create_ex.restype = i32
     L.cltk_plan_create_ex.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t, cp, PO,
                                       C.POINTER(vp), PE]
+    L.cltk_reindex.restype = i32
+    L.cltk_reindex.argtypes = [cp, cp, C.POINTER(vp), PE]
     L.cltk_jit_source.restype = i32
     L.cltk_jit_source.argtypes = [cp, vp, C.c_size_t, C.c_size_t, cp, P64, C.c_size_t, cp, i32, i32,
                                   C.POINTER(vp), PE]

@@ -392,6 +392,15 @@ int cltk_jit_compile(const char* source, uint64_t* cubin_bytes, char** log, cltk
   });
 }
 
+int cltk_reindex(const char* il_json, const char* tenv_json, char** kernel_json, cltk_error* err) {
+  return guarded(err, [&] {
+    const std::string s = kernelToJsonString(kernelFromIL(il_json, tenvOf(tenv_json)));
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.c_str(), s.size() + 1);
+    *kernel_json = p;
+  });
+}
+
 int cltk_plan_dump(const cltk_plan* plan, char** json) {
   std::string s = plan->plan->dump();
   char* p = static_cast<char*>(std::malloc(s.size() + 1));

@@ -68,6 +68,7 @@ struct KNode {
   double real = 0.0;         // FloatLit
   bool boolean = false;      // BoolLit
   int32_t from = -1, to = -1;  // PayRef parties (index into Kernel::partyNames)
+  int32_t wvar = -1;         // LoopIf window's template variable (index into tvars), -1: literal
 };
 
 // Flattened payoff (proj/include/cltk/kernel.hpp:71-79).
@@ -91,6 +92,14 @@ Kernel kernelFromJson(const std::string& json);
 Kernel kernelFromSource(const std::string& text, const std::vector<uint64_t>& tenvValues = {});
 // Either wire format: JSON ('{' first) or kernel text.
 Kernel kernelFromWire(const std::string& text, const std::vector<uint64_t>& tenvValues = {});
+
+class TEnv;
+// reindex (proj/src/kernel.cpp:14-180, :301-303): the IL of a compiled
+// contract (its JSON wire format, ilToJson, proj/src/json_io.cpp:203-303)
+// flattened into a kernel with template variables bound from tenv.
+Kernel kernelFromIL(const std::string& ilJson, const TEnv& tenv);
+// kernelToJson (proj/src/kernel.cpp:520-623), compact.
+std::string kernelToJsonString(const Kernel& k);
 
 // Shape hash: equal for kernels that differ only in FloatLit values (the
 // "template instances" of one contract, priced with shared paths).

@@ -43,7 +43,10 @@ struct KernelReader {
       n.a = read(j.at("cond"));
       n.b = read(j.at("then"));
       n.c = read(j.at("else"));
-      if (n.kind == KKind::LoopIf) n.nat = j.at("window").get<uint64_t>();
+      if (n.kind == KKind::LoopIf) {
+        n.nat = j.at("window").get<uint64_t>();
+        if (j.contains("windowVar")) n.wvar = j.at("windowVar").get<int32_t>();
+      }
     } else if (kind == "float") {
       n.kind = KKind::Float;
       n.real = j.at("value").get<double>();
@@ -433,6 +436,7 @@ struct TextReader {
       if (idx < 0 || static_cast<std::size_t>(idx) >= tenvValues.size())
         fail("loop window tenv[" + std::to_string(idx) + "] has no value");
       n.nat = tenvValues[static_cast<std::size_t>(idx)];
+      n.wvar = static_cast<int32_t>(idx);
     } else {
       double d;
       int64_t w = 0;
