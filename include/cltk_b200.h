@@ -87,7 +87,11 @@ const char* cltk_version(void);
 
 /* priceAcrossTime: results[n_days].  `threads` is accepted and ignored (the
  * reference guarantees identical results for any value).  device < 0: the
- * current CUDA device. */
+ * current CUDA device.  The entry points without cltk_options evaluate the
+ * payoff as jit = 2 does (NVRTC-generated kernel when NVRTC is available;
+ * compiled once per program shape, cached in-process and on disk under
+ * $CLTK_JIT_CACHE_DIR or ~/.cache/cltk_b200; bit-identical to the
+ * interpreter). */
 int cltk_gpu_price(const char* kernel_json, const char* model_json, uint64_t paths,
                    uint64_t seed, const uint64_t* days, size_t n_days, const char* tenv_json,
                    unsigned threads, int device, cltk_price_result* results, cltk_error* err);

@@ -208,7 +208,7 @@ RNG_MODES = {"philox": 0, "sobol": 1}
 JIT_MODES = {False: 0, True: 1, "auto": 2}
 
 
-def _options(device: int = -1, rewrite: bool = True, rng: str = "philox", jit=False):
+def _options(device: int = -1, rewrite: bool = True, rng: str = "philox", jit="auto"):
     if rng not in RNG_MODES:
         raise ValueError(f"rng must be one of {sorted(RNG_MODES)}")
     if jit not in JIT_MODES:
@@ -225,21 +225,22 @@ def version() -> str:
 
 def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, seed: int = 0,
           days: Sequence[int] = (0,), tenv: dict | None = None, threads: int = 0,
-          device: int = -1, rng: str = "philox", jit=False) -> list[dict]:
+          device: int = -1, rng: str = "philox", jit="auto") -> list[dict]:
     """priceAcrossTime on the GPU (cltk.price, proj/python/bindings.cpp:103-126).
 
     Returns one dict per valuation day: ``price``, ``std_error``, ``paths``,
     ``seed``, ``valuation_day``.  ``threads`` is accepted for compatibility
     (results never depend on it).  ``rng="philox"`` (default) reproduces the
     reference's per-path values bit for bit; ``rng="sobol"`` is the QMC mode
-    (Sobol + AS241 + Brownian bridge).  ``jit=True`` evaluates the payoff
-    with the NVRTC-generated kernel instead of the bytecode interpreter
-    (bit-identical results)."""
+    (Sobol + AS241 + Brownian bridge).  ``jit``: ``"auto"`` (default) evaluates
+    the payoff with the NVRTC-generated kernel when NVRTC is available (compiled
+    once per program shape and cached in-process and on disk), ``True`` always,
+    ``False`` with the bytecode interpreter -- bit-identical results."""
     L = _native.lib()
     d, nd = _days(days)
     out = (_native.PriceResultC * max(1, nd))()
     err = _native.ErrorC()
-    if rng == "philox" and not jit:
+    if rng == "philox" and jit == "auto":
         rc = L.cltk_gpu_price(_kernel_json(kernel), _model_json(model), int(paths), int(seed), d,
                               nd, _tenv_json(tenv), int(threads), int(device), out, C.byref(err))
     else:
@@ -253,7 +254,7 @@ def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, s
 
 def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths: int = 100000,
                 seed: int = 0, days: Sequence[int] = (0,), tenv: dict | None = None,
-                device: int = -1, rng: str = "philox", jit=False) -> list[list[dict]]:
+                device: int = -1, rng: str = "philox", jit="auto") -> list[list[dict]]:
     """Price literal instances of one template on one shared path set (no
     recompilation per instance): ``[instance][day]`` result dicts."""
     L = _native.lib()
@@ -262,7 +263,7 @@ def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths
     arr = (C.c_char_p * n)(*[_kernel_json(k) for k in kernels])
     out = (_native.PriceResultC * max(1, n * nd))()
     err = _native.ErrorC()
-    if rng == "philox" and not jit:
+    if rng == "philox" and jit == "auto":
         rc = L.cltk_gpu_price_batch(arr, n, _model_json(model), int(paths), int(seed), d, nd,
                                     _tenv_json(tenv), int(device), out, C.byref(err))
     else:
@@ -290,7 +291,7 @@ def kernel_literals(kernel: Kernel | str | dict) -> list[float]:
 def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
                    paths: int = 100000, seed: int = 0, days: Sequence[int] = (0,),
                    tenv: dict | None = None, device: int = -1,
-                   rng: str = "philox", jit=False) -> list[list[dict]]:
+                   rng: str = "philox", jit="auto") -> list[list[dict]]:
     """Price instances of one template given as a literal table
     ``literals[instance][j]`` (j in ``kernel_literals`` order): one compile,
     one path set, the literals passed to the kernel as data."""

@@ -51,7 +51,7 @@ def main(argv=None) -> int:
     p.add_argument("--threads", type=int, default=0, help="accepted; results never depend on it")
     p.add_argument("--tenv")
     p.add_argument("--rng", default="philox", choices=["philox", "sobol"])
-    p.add_argument("--jit", default="0", choices=["0", "1", "auto"])
+    p.add_argument("--jit", default="auto", choices=["0", "1", "auto"])
     p.add_argument("--device", type=int, default=-1)
     args = ap.parse_args(argv)
     try:

@@ -154,8 +154,10 @@ struct RunOptions {
   int rng = 0;
   // Payoff evaluation: 0 = bytecode interpreter (ahead-of-time kernel),
   // 1 = NVRTC-generated kernel (jit.cpp; error if NVRTC is unavailable),
-  // 2 = NVRTC when available and the program is small enough, else 0.
-  int jit = 0;
+  // 2 = NVRTC when available and the program is small enough, else 0
+  // (default: the one-shot entry points price with the generated kernel,
+  // compiled once per program shape and cached in-process and on disk).
+  int jit = 2;
 };
 
 // ---- compiled plan (host + device state) ------------------------------------

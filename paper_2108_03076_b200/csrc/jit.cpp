@@ -6,6 +6,7 @@
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <unistd.h>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -532,22 +533,103 @@ size_t jitCompileOnly(const std::string& src, std::string* log) {
   return compileCubin(src, log).size();
 }
 
+namespace {
+// On-disk cubin cache (best effort): a program compiled once on a machine is
+// loaded by later processes without NVRTC.  Keyed by the generated source,
+// the embedded engine headers and the extra NVRTC flags (FNV-1a 64).
+// Directory: $CLTK_JIT_CACHE_DIR, else $XDG_CACHE_HOME/cltk_b200, else
+// $HOME/.cache/cltk_b200; CLTK_JIT_CACHE_DIR="" disables it.
+uint64_t fnv1a(uint64_t h, const std::string& s) {
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 0x100000001B3ULL;
+  }
+  return h;
+}
+std::string cacheDir() {
+  if (const char* d = std::getenv("CLTK_JIT_CACHE_DIR")) return d;
+  if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) return std::string(x) + "/cltk_b200";
+  if (const char* h = std::getenv("HOME"); h && *h) return std::string(h) + "/.cache/cltk_b200";
+  return "";
+}
+std::string cachePath(const std::string& src) {
+  const std::string dir = cacheDir();
+  if (dir.empty()) return "";
+  uint64_t h = fnv1a(0xCBF29CE484222325ULL, src);
+  for (int i = 0; i < kJitHeaderCount; ++i) h = fnv1a(h, kJitHeaderSources[i]);
+  if (const char* f = std::getenv("CLTK_JIT_FLAGS")) h = fnv1a(h, f);
+  char name[40];
+  std::snprintf(name, sizeof name, "/%016llx.cubin", static_cast<unsigned long long>(h));
+  return dir + name;
+}
+bool readFile(const std::string& path, std::vector<uint8_t>* out) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  std::fseek(f, 0, SEEK_END);
+  const long n = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  out->resize(n > 0 ? static_cast<size_t>(n) : 0);
+  const bool ok = n > 0 && std::fread(out->data(), 1, out->size(), f) == out->size();
+  std::fclose(f);
+  return ok;
+}
+void writeFileAtomic(const std::string& path, const std::vector<uint8_t>& data) {
+  const std::string dir = path.substr(0, path.rfind('/'));
+  std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
+  if (std::system(mk.c_str()) != 0) return;
+  const std::string tmp = path + ".tmp" + std::to_string(static_cast<long>(getpid()));
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const bool ok = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+  std::fclose(f);
+  if (!ok || std::rename(tmp.c_str(), path.c_str()) != 0) std::remove(tmp.c_str());
+}
+}  // namespace
+
+namespace {
+// Load a cubin and find the path kernel; false (error in *e) if either fails.
+bool loadKernel(const std::vector<uint8_t>& cubin, cudaKernel_t* k, cudaError_t* e,
+                const char** what) {
+  cudaLibrary_t lib;
+  *what = "cudaLibraryLoadData";
+  *e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (*e != cudaSuccess) return false;
+  *what = "cudaLibraryGetKernel";
+  *e = cudaLibraryGetKernel(k, lib, "cltk_jit_path");
+  if (*e != cudaSuccess) {
+    cudaLibraryUnload(lib);
+    return false;
+  }
+  return true;
+}
+bool looksLikeCubin(const std::vector<uint8_t>& b) {
+  return b.size() > 64 && b[0] == 0x7f && b[1] == 'E' && b[2] == 'L' && b[3] == 'F';
+}
+}  // namespace
+
 const void* jitKernel(const std::string& src) {
   static std::mutex mu;
   static std::unordered_map<std::string, cudaKernel_t> cache;
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(src);
   if (it != cache.end()) return reinterpret_cast<const void*>(it->second);
-  std::string log;
-  std::vector<uint8_t> cubin = compileCubin(src, &log);
-  cudaLibrary_t lib;
-  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e != cudaSuccess)
-    throw DeviceError(std::string("jit: cudaLibraryLoadData: ") + cudaGetErrorString(e));
+  const std::string path = cachePath(src);
+  std::vector<uint8_t> cubin;
   cudaKernel_t k;
-  e = cudaLibraryGetKernel(&k, lib, "cltk_jit_path");
-  if (e != cudaSuccess)
-    throw DeviceError(std::string("jit: cudaLibraryGetKernel: ") + cudaGetErrorString(e));
+  cudaError_t e = cudaSuccess;
+  const char* what = "";
+  // a cached cubin is used only if it is an ELF image that loads and holds the
+  // kernel; anything else (stale, damaged) is recompiled and rewritten
+  bool ok = !path.empty() && readFile(path, &cubin) && looksLikeCubin(cubin) &&
+            loadKernel(cubin, &k, &e, &what);
+  if (!ok) {
+    cudaGetLastError();  // clear a failed load of a damaged entry
+    std::string log;
+    cubin = compileCubin(src, &log);
+    if (!path.empty()) writeFileAtomic(path, cubin);
+    if (!loadKernel(cubin, &k, &e, &what))
+      throw DeviceError(std::string("jit: ") + what + ": " + cudaGetErrorString(e));
+  }
   cache.emplace(src, k);
   return reinterpret_cast<const void*>(k);
 }

@@ -8,6 +8,7 @@ GPU: prices through the NVRTC kernel equal the interpreter's bit for bit --
 same ops, same order, same IEEE operations -- for every golden case, both RNG
 modes, template batches and literal tables, and the error channel.
 """
+import os
 import re
 
 import numpy as np
@@ -174,3 +175,30 @@ def test_log_domain_extrema_bitwise_vs_interpreter(variant):
         b = E.price(k, m, 40000, 7, [0, 100, 300], rng=rng, jit=True)
         for x, y in zip(a, b):
             assert x["price"] == y["price"] and x["std_error"] == y["std_error"], (rng, x, y)
+
+
+@pytest.mark.gpu
+def test_disk_cache_reuses_and_repairs_the_cubin(tmp_path):
+    """The NVRTC cubin of a program is written to CLTK_JIT_CACHE_DIR and loaded
+    by a later process; a damaged entry is recompiled, never trusted."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.setrecursionlimit(100000); import paper_2108_03076_b200 as E, json;"
+            "from conftest import load_kernel, load_model;"
+            "r = E.price(E.Kernel(load_kernel('worst-off')), load_model('three'), 4096, 5, jit=True);"
+            "print(json.dumps(r[0]['price'].hex()))")
+    env = dict(os.environ, CLTK_JIT_CACHE_DIR=str(tmp_path))
+    here = os.path.dirname(os.path.abspath(__file__))
+    env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, env.get("PYTHONPATH", "")])
+    run = lambda: subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                                 text=True, timeout=300)
+    a = run()
+    assert a.returncode == 0, a.stderr
+    files = list(tmp_path.glob("*.cubin"))
+    assert len(files) == 1 and files[0].stat().st_size > 0
+    b = run()
+    assert b.returncode == 0 and b.stdout == a.stdout
+    files[0].write_bytes(b"not a cubin")
+    c = run()
+    assert c.returncode == 0 and c.stdout == a.stdout, c.stderr
+    assert files[0].read_bytes() != b"not a cubin"
