@@ -106,6 +106,7 @@ struct PlanImpl {
   uint32_t nOut = 0;
   const void* jitFn = nullptr;  // NVRTC kernel (cudaKernel_t) or null: interpreter
   uint64_t drawsPerPath = 0;    // normals per path (chunk sizing)
+  uint32_t pathBatch = 1;       // paths per normal batch (ppt is a multiple of it)
 
   ~PlanImpl() {
     int cur = 0;
@@ -166,6 +167,10 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   I.nOut = I.prog.header.n_instances * I.prog.header.n_days;
   for (const cltk_step& st : I.prog.steps)
     if (st.draws == 1) I.drawsPerPath += I.prog.header.n_assets;
+  // path batches (engine_types.h pathBatch): normal slots per path = steps x assets
+  I.pathBatch = I.prog.header.rng == CLTK_RNG_PHILOX
+                    ? pathBatch(I.prog.header.n_steps * std::max<uint32_t>(1, I.prog.header.n_assets))
+                    : 1;
   if (opt.jit < 0 || opt.jit > 2) throw UnsupportedError("unknown jit mode");
   std::string jitSrc;
   if (opt.jit != JIT_OFF) {
@@ -266,6 +271,10 @@ void Plan::chunking(uint64_t paths, uint64_t* chunkPaths, uint64_t* nChunks) con
   const uint64_t pptBalance = std::max<uint64_t>(1, paths / (kBlock * 8192ull));
   ppt = std::max<uint64_t>(ppt, std::min(pptWork, pptBalance));
   ppt = std::max<uint64_t>(1, ppt);
+  // whole path batches per thread (a function of the program: the interpreted
+  // and the generated kernel chunk alike, so their results stay bit-identical)
+  const uint64_t pb = impl_->pathBatch;
+  ppt = (ppt + pb - 1) / pb * pb;
   *chunkPaths = ppt * kBlock;
   *nChunks = (paths + *chunkPaths - 1) / *chunkPaths;
 }

@@ -12,6 +12,23 @@ namespace b200 {
 constexpr int kBlock = 128;  // threads per CTA (4 warps)
 constexpr int kWarps = kBlock / 32;
 
+// Normal draws per thread of one warp-cooperative batch (engine_device.cuh).
+#ifndef CLTK_MAX_BATCH
+#define CLTK_MAX_BATCH 6
+#endif
+// Short paths (Philox mode, at most half a batch of draws per path): one
+// batch draws the normals of pathBatch consecutive paths of a thread, so the
+// batch's fixed costs (barriers, pooled passes) are shared.  A function of the
+// program only (draws = steps x assets, every step's slots counted).
+#if defined(__CUDACC__)
+#define CLTK_TYPES_HD __host__ __device__
+#else
+#define CLTK_TYPES_HD
+#endif
+CLTK_TYPES_HD inline constexpr uint32_t pathBatch(uint32_t draws) {
+  return (draws >= 1 && 2 * draws <= CLTK_MAX_BATCH) ? CLTK_MAX_BATCH / draws : 1;
+}
+
 // Philox2x64-10 key schedule key_r = seed + r * 0x9E3779B97F4A7C15.
 struct PhiloxKeys {
   uint64_t k[10];
