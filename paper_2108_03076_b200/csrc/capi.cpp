@@ -60,6 +60,28 @@ TEnv tenvOf(const char* j) { return (j && *j) ? tenvFromJson(j) : TEnv{}; }
 
 }  // namespace
 
+namespace {
+// Plan-cache key of a one-shot call: every wire input, the options and the
+// resolved device (engine.cpp priceCached).
+struct KeyBuilder {
+  std::string key;
+  void add(const void* p, size_t n) { key.append(static_cast<const char*>(p), n); }
+  void str(const char* s) {
+    const size_t n = s ? std::strlen(s) : 0;
+    add(&n, sizeof n);
+    if (n) add(s, n);
+  }
+  template <class T>
+  void val(const T& v) { add(&v, sizeof v); }
+};
+int resolvedDevice(int device) {
+  if (device >= 0) return device;
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+}  // namespace
+
 extern "C" {
 
 const char* cltk_version(void) { return "cltk-b200 0.1 (sm_100a)"; }
@@ -70,18 +92,31 @@ double cltk_black_scholes_call(double spot, double strike, double rate, double v
   return blackScholesCall(spot, strike, rate, vol, t);
 }
 
+
 int cltk_gpu_price(const char* kernel_json, const char* model_json, uint64_t paths, uint64_t seed,
                    const uint64_t* days, size_t n_days, const char* tenv_json, unsigned threads,
                    int device, cltk_price_result* results, cltk_error* err) {
   return guarded(err, [&] {
     if (paths == 0) throw EvalError("path count must be positive");
-    Kernel k = kernelFromWire(kernel_json);
-    ModelSpec m = modelFromJson(model_json);
     std::vector<uint64_t> d(days, days + n_days);
     RunOptions opt;
     opt.device = device;
     (void)threads;
-    auto r = priceBatch({&k}, m, paths, seed, d, tenvOf(tenv_json), opt);
+    KeyBuilder kb;
+    kb.str("cltk_gpu_price");
+    kb.str(kernel_json);
+    kb.str(model_json);
+    kb.str(tenv_json);
+    kb.add(d.data(), d.size() * sizeof(uint64_t));
+    kb.val(resolvedDevice(device));
+    auto r = priceCached(
+        kb.key,
+        [&] {
+          const Kernel k = kernelFromWire(kernel_json);
+          return std::make_unique<Plan>(std::vector<const Kernel*>{&k},
+                                        modelFromJson(model_json), d, tenvOf(tenv_json), opt);
+        },
+        paths, seed, d);
     toC(r, results);
   });
 }
@@ -168,20 +203,39 @@ int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_
                       const cltk_options* opts, cltk_price_result* results, cltk_error* err) {
   return guarded(err, [&] {
     if (paths == 0) throw EvalError("path count must be positive");
-    Kernel k = kernelFromWire(kernel_json);
-    ModelSpec m = modelFromJson(model_json);
     std::vector<uint64_t> d(days, days + n_days);
-    RunOptions opt = optionsOf(opts);
-    std::vector<double> own;
-    if (!literals) {
-      own = kernelFloatLiterals(k);
-      literals = own.data();
-      n_instances = 1;
-      n_literals = own.size();
-    }
-    toC(priceTemplate(k, literals, n_instances, n_literals, m, paths, seed, d, tenvOf(tenv_json),
-                      opt),
-        results);
+    const RunOptions opt = optionsOf(opts);
+    KeyBuilder kb;
+    kb.str("cltk_gpu_price_ex");
+    kb.str(kernel_json);
+    kb.str(model_json);
+    kb.str(tenv_json);
+    kb.add(d.data(), d.size() * sizeof(uint64_t));
+    kb.val(resolvedDevice(opt.device));
+    kb.val(opt.rewrite);
+    kb.val(opt.rng);
+    kb.val(opt.jit);
+    kb.val(n_instances);
+    kb.val(n_literals);
+    if (literals) kb.add(literals, n_instances * n_literals * sizeof(double));
+    auto r = priceCached(
+        kb.key,
+        [&] {
+          const Kernel k = kernelFromWire(kernel_json);
+          std::vector<double> own;
+          const double* lit = literals;
+          size_t ni = n_instances, nl = n_literals;
+          if (!lit) {
+            own = kernelFloatLiterals(k);
+            lit = own.data();
+            ni = 1;
+            nl = own.size();
+          }
+          return std::make_unique<Plan>(k, lit, ni, nl, modelFromJson(model_json), d,
+                                        tenvOf(tenv_json), opt);
+        },
+        paths, seed, d);
+    toC(r, results);
   });
 }
 

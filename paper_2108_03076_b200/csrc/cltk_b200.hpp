@@ -17,6 +17,7 @@
 // nothing (results are bit-identical for any value, as in the reference).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -233,6 +234,14 @@ std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* litera
                                        const ModelSpec& model, uint64_t paths, uint64_t seed,
                                        const std::vector<uint64_t>& days, const TEnv& tenv,
                                        const RunOptions& opt = RunOptions());
+// One-shot pricing through an in-process plan cache (the last few plans,
+// keyed by the caller's exact wire inputs, options and device): a repeated
+// call skips parsing, compiling and uploading.  make() builds the plan on a
+// miss.  Plans in the cache are used by one caller at a time.
+std::vector<PriceResult> priceCached(const std::string& key,
+                                     const std::function<std::unique_ptr<Plan>()>& make,
+                                     uint64_t paths, uint64_t seed,
+                                     const std::vector<uint64_t>& days);
 // Template batch: instances share one path set (common random numbers, like
 // repeated reference calls with one seed); result [instance * days + d].
 std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,

@@ -568,6 +568,56 @@ std::vector<PriceResult> oneShot(MakePlan make, uint64_t paths, uint64_t seed,
 }
 }  // namespace
 
+std::vector<PriceResult> priceCached(const std::string& key,
+                                     const std::function<std::unique_ptr<Plan>()>& make,
+                                     uint64_t paths, uint64_t seed,
+                                     const std::vector<uint64_t>& days) {
+  struct Entry {
+    std::string key;
+    std::unique_ptr<Plan> plan;
+    std::mutex use;
+  };
+  constexpr size_t kEntries = 4;
+  static std::mutex mu;
+  static std::vector<std::shared_ptr<Entry>> lru;  // most recent last
+  if (paths == 0) throw EvalError("path count must be positive");
+  if (days.empty()) {  // nothing to price; the inputs are still validated
+    (void)make();
+    return {};
+  }
+  std::shared_ptr<Entry> e;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (size_t i = 0; i < lru.size(); ++i)
+      if (lru[i]->key == key) {
+        e = lru[i];
+        lru.erase(lru.begin() + static_cast<std::ptrdiff_t>(i));
+        lru.push_back(e);
+        break;
+      }
+  }
+  if (!e) {
+    e = std::make_shared<Entry>();
+    e->key = key;
+    e->plan = make();
+    std::lock_guard<std::mutex> lock(mu);
+    lru.push_back(e);
+    if (lru.size() > kEntries) lru.erase(lru.begin());
+  }
+  std::lock_guard<std::mutex> use(e->use);
+  try {
+    return runOnce(*e->plan, paths, seed, days);
+  } catch (...) {  // a plan that failed on the device is not reused
+    std::lock_guard<std::mutex> lock(mu);
+    for (size_t i = 0; i < lru.size(); ++i)
+      if (lru[i] == e) {
+        lru.erase(lru.begin() + static_cast<std::ptrdiff_t>(i));
+        break;
+      }
+    throw;
+  }
+}
+
 std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,
                                     const ModelSpec& model, uint64_t paths, uint64_t seed,
                                     const std::vector<uint64_t>& days, const TEnv& tenv,
