@@ -218,6 +218,9 @@ def main():
     args = ap.parse_args()
     args.jit = {"0": False, "1": True, "auto": "auto"}[args.jit]
 
+    # the e2e calls build their plan every time (parse, compile, upload): no
+    # in-process plan cache between timed calls
+    os.environ["CLTK_PLAN_CACHE"] = "0"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -383,6 +386,7 @@ def main():
                 "e2e": {"value": paths * n_inst / t_e2e if t_e2e > 0 else None, "unit": "paths/s",
                         "h2d_bytes_per_step": h2d, "samples_ms": [round(t * 1e3, 3) for t in e2e_times],
                         "statistic": "median of the timed calls",
+                        "plan_cache": "off (every call parses, compiles and uploads its plan)",
                         "d2h_bytes_per_step": d2h, "clocks": clk_e2e,
                         "path": "paper_2108_03076_b200.price -> cltk_gpu_price[_ex] (C-ABI), host "
                                 "kernel/model JSON in, host results out"},

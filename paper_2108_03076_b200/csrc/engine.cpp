@@ -585,6 +585,15 @@ std::vector<PriceResult> priceCached(const std::string& key,
     (void)make();
     return {};
   }
+  // CLTK_PLAN_CACHE=0: every call builds (parses, compiles, uploads) its plan
+  static const bool enabled = [] {
+    const char* v = std::getenv("CLTK_PLAN_CACHE");
+    return v == nullptr || std::strcmp(v, "0") != 0;
+  }();
+  if (!enabled) {
+    std::unique_ptr<Plan> plan = make();
+    return runOnce(*plan, paths, seed, days);
+  }
   std::shared_ptr<Entry> e;
   {
     std::lock_guard<std::mutex> lock(mu);
