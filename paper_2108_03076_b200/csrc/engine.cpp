@@ -167,6 +167,10 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   I.nOut = I.prog.header.n_instances * I.prog.header.n_days;
   for (const cltk_step& st : I.prog.steps)
     if (st.draws == 1) I.drawsPerPath += I.prog.header.n_assets;
+  // Philox draw indices are 32-bit on the device (engine_device.cuh philox_keyed32)
+  if (static_cast<uint64_t>(I.prog.header.n_steps) * std::max<uint32_t>(1, I.prog.header.n_assets) >=
+      (1ULL << 32))
+    throw UnsupportedError("more than 2^32 normal draws per path");
   // path batches (engine_types.h pathBatch): normal slots per path = steps x assets
   I.pathBatch = I.prog.header.rng == CLTK_RNG_PHILOX
                     ? pathBatch(I.prog.header.n_steps * std::max<uint32_t>(1, I.prog.header.n_assets))
