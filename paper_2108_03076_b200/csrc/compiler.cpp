@@ -1184,6 +1184,7 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   h.n_assets = nA;
   h.n_steps = nSteps;
   h.n_thread = nThread;
+  h.reg_top = nThread;
   h.n_shared_const = static_cast<uint32_t>(P.sharedConst.size());
   h.n_inst_const = nInstC;
   h.n_instances = static_cast<uint32_t>(nInst);

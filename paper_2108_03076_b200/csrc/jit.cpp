@@ -5,6 +5,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <unistd.h>
 #include <cstdlib>
@@ -529,7 +530,23 @@ std::string jitSource(CompiledProgram& prog) {
         "  cltk::b200::path_body<"
      << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false") << ", cltk::b200::JitPayoff, "
      << pb << ", " << (pb > 1 ? slots : 0) << ">(P, A, accInSmem);\n}\n";
-  return os.str();
+  // Shared-memory register columns: only the registers the generated code
+  // stores or loads (JW / JR) or the outputs read; the rest live in locals.
+  std::string src = os.str();
+  uint32_t top = prog.header.reg_base;
+  for (const char* pat : {"JR(", "JW("}) {
+    for (size_t at = src.find(pat); at != std::string::npos; at = src.find(pat, at + 3)) {
+      const char* q = src.c_str() + at + 3;
+      if (*q < '0' || *q > '9') continue;  // the macro definitions
+      top = std::max<uint32_t>(top, static_cast<uint32_t>(std::strtoul(q, nullptr, 10)) + 1);
+    }
+  }
+  for (const cltk_output& o : prog.outputs) {
+    if (o.val < h.n_thread) top = std::max(top, o.val + 1);
+    if (o.err != CLTK_NO_ERR && o.err < h.n_thread) top = std::max(top, o.err + 1);
+  }
+  prog.header.reg_top = std::min<uint32_t>(top, h.n_thread);
+  return src;
 }
 
 size_t jitCompileOnly(const std::string& src, std::string* log) {

@@ -66,7 +66,7 @@ bool accFitsSmem(const cltk_plan_header& h) {
 
 size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
   const size_t nOut = static_cast<size_t>(h.n_instances) * h.n_days;
-  size_t words = static_cast<size_t>(h.n_thread - h.reg_base) * kBlock +
+  size_t words = static_cast<size_t>(h.reg_top - h.reg_base) * kBlock +
                  kWarps * (h.n_shared_const + h.n_inst_const);
   if (accInSmem) words += kWarps * nOut * 3;
   words += kWarps + 1;  // counts + chunk slot

@@ -120,6 +120,8 @@ typedef struct {
   uint32_t n_bridge_ops;    // QMC: computes (= drawing steps)
   uint32_t reg_base;        // path kernel: leading operand slots without shared-memory
                             // columns (the NVRTC kernel keeps the S-slots in registers)
+  uint32_t reg_top;         // path kernel: operand slots [reg_base, reg_top) have columns
+                            // (n_thread; the NVRTC kernel: only the registers it stores)
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
