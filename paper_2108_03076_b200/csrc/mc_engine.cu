@@ -38,7 +38,8 @@ template <int NA, bool QMC>
 cudaError_t launchDumpT(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
   const cltk_plan_header& h = p.hdr;
   size_t smem = (static_cast<size_t>(h.n_thread) * kBlock +
-                 kWarps * (h.n_shared_const + h.n_inst_const) + normScratchWords(h.n_assets ? h.n_assets : 1) +
+                 kWarps * (h.n_shared_const + h.n_inst_const) +
+                 normScratchWords(h.n_assets ? h.n_assets : 1, h.rng == CLTK_RNG_SOBOL) +
                  bridgeWords(h)) *
                 sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(dump_kernel<NA, QMC>,
@@ -70,7 +71,7 @@ size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
                  kWarps * (h.n_shared_const + h.n_inst_const);
   if (accInSmem) words += kWarps * nOut * 3;
   words += kWarps + 1;  // counts + chunk slot
-  words += normScratchWords(h.n_assets ? h.n_assets : 1);
+  words += normScratchWords(h.n_assets ? h.n_assets : 1, h.rng == CLTK_RNG_SOBOL);
   words += bridgeWords(h);
   return words * sizeof(double);
 }
