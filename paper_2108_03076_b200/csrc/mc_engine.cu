@@ -30,7 +30,7 @@ cudaError_t launchPathT(const DevPlan& p, const RunArgs& a, int grid, size_t sme
 size_t bridgeWords(const cltk_plan_header& h) {
   if (h.rng != CLTK_RNG_SOBOL) return 0;
   const size_t need = static_cast<size_t>(h.n_bridge_slots) * (h.n_assets ? h.n_assets : 1) * kBlock;
-  const size_t have = static_cast<size_t>(batchSlots(h.n_assets ? h.n_assets : 1)) * kBlock;  // the Y slots
+  const size_t have = static_cast<size_t>(yRows(h.n_assets ? h.n_assets : 1, true)) * kBlock;  // the Y rows
   return need > have ? need - have : 0;
 }
 
