@@ -46,7 +46,7 @@ F_PATH_QMC = {"brc": 102669.7}
 # its ~90 KB program and the partials stay in L2), and the FP64 pipe activity
 # ncu measured there -- the kernel's own pipe utilisation beside the frozen-F
 # roofline fraction.
-NCU_EVIDENCE = {"brc": {"traffic": 214528.0, "fp64_pipe_active": 0.471,
+NCU_EVIDENCE = {"brc": {"traffic": 222720.0, "fp64_pipe_active": 0.470,
                         "capture": "profiles/r1j_path_kernel_brc_10M_raw.csv (10M-path launch)"}}
 
 BATCH_N = 1024
