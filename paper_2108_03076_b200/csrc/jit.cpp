@@ -525,7 +525,8 @@ std::string jitSource(CompiledProgram& prog) {
         "                                              uint32_t inst) {\n";
   g.emit(os, instOps, false, instBlock, "    ");
   os << "  }\n};\n}  // namespace\n}  // namespace b200\n}  // namespace cltk\n"
-        "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, CLTK_MIN_BLOCKS)\n"
+        "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, "
+     << (h.rng == CLTK_RNG_SOBOL ? "CLTK_QMC_MIN_BLOCKS" : "CLTK_MIN_BLOCKS") << ")\n"
         "cltk_jit_path(const cltk::b200::DevPlan P, const cltk::b200::RunArgs A, int accInSmem) {\n"
         "  cltk::b200::path_body<"
      << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false") << ", cltk::b200::JitPayoff, "
