@@ -15,7 +15,7 @@ CXXFLAGS := -std=c++17 -O2 -fPIC -ffp-contract=off -Wall -Wno-unused-function \
 NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -ccbin $(HOSTCXX) \
             -Xcompiler -fPIC -Xptxas -v -Iinclude
 
-HOST_SRCS := host_model compiler engine capi sobol_table jit reindex
+HOST_SRCS := host_model compiler engine capi sobol_table jit reindex nccl_comm
 HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS))) $(OBJ)/jit_sources.o
 # device headers embedded for the NVRTC build (csrc/jit.cpp)
 JIT_HDRS  := $(SRC)/engine_device.cuh $(SRC)/engine_types.h $(SRC)/program.h \

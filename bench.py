@@ -10,7 +10,9 @@ A step = one full pricing pass (simulate + payoff + reduce) over
 paths_per_gpu * N paths of the BRC kernel (weak scaling), inputs (the compiled
 program) resident on the device.  N > 1 runs one process per GPU under
 torch.distributed (NCCL); the only data-path collective is the single
-all_reduce of the chunk partials.  Rank 0 prints ONE JSON line.
+all-gather of the chunk partials.  `--gpus N` without torchrun re-launches
+itself under `torch.distributed.run --nproc-per-node N`.  Rank 0 prints ONE
+JSON line.
 """
 from __future__ import annotations
 
@@ -221,18 +223,38 @@ def main():
     # the e2e calls build their plan every time (parse, compile, upload): no
     # in-process plan cache between timed calls
     os.environ["CLTK_PLAN_CACHE"] = "0"
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.impl == "b200" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's own launch
+        # already sets WORLD_SIZE)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        argv = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank)
         return
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}: launch one "
+                         "process per GPU (torchrun --nproc-per-node N) or drop WORLD_SIZE")
 
     import torch
     import torch.distributed as dist
     import paper_2108_03076_b200 as E
-    from paper_2108_03076_b200.distributed import DistributedPricer
+    from paper_2108_03076_b200.distributed import DistributedPricer, gather_partials_
 
+    visible = torch.cuda.device_count()
+    if local >= visible:
+        raise SystemExit(f"bench: rank {rank} needs GPU {local} but only {visible} visible")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -259,6 +281,8 @@ def main():
 
     for _ in range(args.warmup):
         pricer.finalize(paths, seed, pricer.launch(paths, seed))
+    # multi-GPU: every rank must price the same bits as one GPU would
+    check = pricer.finalize(paths, seed, pricer.launch(paths, seed))
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -274,14 +298,9 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        _, nc = pricer.plan.chunking(paths)
-        parts = pricer.partials(paths)
-        parts.zero_()
-        c0, c1 = nc * rank // world, nc * (rank + 1) // world
-        pricer.plan.launch(paths, seed, c0, c1, parts.data_ptr(), stream.cuda_stream)
+        parts = pricer.launch_local(paths, seed, stream.cuda_stream)  # this rank's chunk slice
         e1.record(stream)
-        if world > 1:
-            dist.all_reduce(parts, op=dist.ReduceOp.SUM)
+        gather_partials_(parts)  # the one data-path collective (NCCL all-gather)
         res = pricer.finalize(paths, seed, parts)  # combine + read-back (synchronises)
         e2.record(stream)
         e2.synchronize()
@@ -325,6 +344,8 @@ def main():
         tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt[0])
+    if [r["price"] for r in res] != [r["price"] for r in check]:
+        raise SystemExit("bench: timed step priced different bits than the check step")
     # our kernels per timed step: the path kernel + the fixed-order combine
     # (two launches when the chunk count is split, engine_launch.hpp kCombineSplit)
     n_chunks = pricer.plan.chunking(paths)[1]
@@ -378,7 +399,8 @@ def main():
                            else "sobol (Joe-Kuo) + AS241 + Brownian bridge (QMC)",
                            "payoff": "NVRTC-generated sm_100a kernel" if info["jit"]
                            else "bytecode interpreter (ahead-of-time kernel)",
-                           "parallelism": f"paths sharded over {world} GPU(s), 1 all_reduce",
+                           "parallelism": f"paths sharded over {world} GPU(s) (one process "
+                                          "each), 1 NCCL all-gather of the chunk partials",
                            "l2": "flushed between timed steps (256 MiB write); inputs are a "
                                  f"{h2d} B compiled program",
                            "kernel_ms": t_kern},

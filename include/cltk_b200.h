@@ -75,18 +75,33 @@ typedef struct {
  * data, so new template instances do not recompile; error if NVRTC is
  * unavailable), 2 = NVRTC when available and the program is small, else 0.
  * Both give bit-identical results. */
+#define CLTK_MAX_DEVICES 16
 typedef struct {
   int device;   /* -1: current */
   int rewrite;  /* default 1 */
   int rng;      /* default 0 */
   int jit;      /* default 0 */
-  int reserved[4];
+  /* n_devices > 0: the one-shot entry points shard the call over
+   * devices[0 .. n_devices) of this process -- a plan per GPU, contiguous
+   * equal slices of the deterministic chunks, ONE NCCL all-gather of the
+   * chunk partials over NVLink (libnccl.so.2, loaded on first use), the
+   * fixed-order combine on devices[0]: bit-identical to one GPU (the
+   * reference's thread-count invariance, proj/src/pricing.cpp:268-286).
+   * A device listed twice shares its GPU (gathered with device copies).
+   * n_devices = 0 and device < 0: $CLTK_DEVICES ("all" or "0,1,...") when
+   * set, else the current device. */
+  int n_devices;
+  int devices[CLTK_MAX_DEVICES];
+  /* test builds only: plans carry the fault hook (cltk_plan_set_fault) */
+  int fault_inject;
+  int reserved[3];
 } cltk_options;
 
 const char* cltk_version(void);
 
 /* priceAcrossTime: results[n_days].  `threads` is accepted and ignored (the
  * reference guarantees identical results for any value).  device < 0: the
+ * GPUs $CLTK_DEVICES lists (sharded as cltk_options.devices), else the
  * current CUDA device.  The entry points without cltk_options evaluate the
  * payoff as jit = 2 does (NVRTC-generated kernel when NVRTC is available;
  * compiled once per program shape, cached in-process and on disk under
@@ -166,7 +181,10 @@ int cltk_plan_chunking(const cltk_plan* plan, uint64_t paths, uint64_t* chunk_pa
                        uint64_t* n_chunks);
 /* Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream):
  * price chunks [c0, c1) into partials_dev[c][out] (device memory of
- * n_chunks * n_outputs cltk_partial_t). */
+ * n_chunks * n_outputs cltk_partial_t).  A plan's launches and its finalize
+ * must be ordered (one stream, or synchronised by the caller): they share
+ * the plan's chunk scheduler counter and device error word.  Concurrent
+ * callers use one plan each. */
 int cltk_plan_launch(cltk_plan* plan, uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1,
                      void* partials_dev, void* stream, cltk_error* err);
 /* Fixed-order combine of partials_dev[0, n_chunks), synchronous read-back,
@@ -178,6 +196,14 @@ int cltk_plan_finalize(cltk_plan* plan, uint64_t paths, uint64_t seed, const voi
  * it, and overwrite it (e.g. with the MIN over ranks) before finalize. */
 int cltk_plan_error_word(cltk_plan* plan, void* stream, uint64_t* word);
 int cltk_plan_set_error_word(cltk_plan* plan, void* stream, uint64_t word);
+/* Test hook: plans created with cltk_options.fault_inject = 1 (Philox mode)
+ * force the uniform of draw `draw` of path `path` to exactly 1.0 in later
+ * launches -- the reference's reachable invNormalCdf domain error
+ * (proj/src/pricing.cpp:100-103,111-113) at a chosen place.  path = ~0: none. */
+int cltk_plan_set_fault(cltk_plan* plan, uint64_t path, uint32_t draw, cltk_error* err);
+/* The NCCL the multi-GPU path loads: *version = ncclGetVersion's code, or
+ * an error when libnccl.so.2 cannot be loaded. */
+int cltk_nccl_version(int* version, cltk_error* err);
 /* Host-only: compile (no device needed) and return the program listing --
  * the engine's analogue of emitKernelSource (proj/src/kernel.cpp:407). */
 int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
@@ -214,6 +240,12 @@ int cltk_debug_rng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64
  * quotient written to both slots); fn = 5: its -x / sqrt(2.0). */
 int cltk_debug_math(int device, int fn, const double* x, uint64_t n, double* out,
                     cltk_error* err);
+/* QMC generator: the 32-bit Sobol integers (Joe-Kuo direction numbers, gray
+ * code) of points [n0, n0 + n), dimensions [d0, d0 + nd), out[n][nd] (host
+ * buffer), from the device code the QMC path kernel runs; aligned = 1 uses
+ * its warp-cooperative skip-ahead (n0 a multiple of 32), 0 the per-point one. */
+int cltk_debug_sobol(int device, uint64_t n0, uint64_t n, uint32_t d0, uint32_t nd, int aligned,
+                     uint32_t* out, cltk_error* err);
 /* Measured DFMA throughput (TFLOP/s) over `iters` iterations. */
 int cltk_fp64_peak(int device, int iters, double* tflops, double* seconds, cltk_error* err);
 

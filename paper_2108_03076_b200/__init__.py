@@ -37,6 +37,7 @@ __all__ = [
     "ContractUnsupportedError", "price", "price_batch", "black_scholes_call", "Plan",
     "compile_listing", "debug_rng", "debug_math", "fp64_peak", "load_kernel", "version",
     "kernel_literals", "price_template", "jit_source", "jit_compile", "reindex",
+    "debug_sobol", "nccl_version",
 ]
 
 
@@ -208,7 +209,8 @@ RNG_MODES = {"philox": 0, "sobol": 1}
 JIT_MODES = {False: 0, True: 1, "auto": 2}
 
 
-def _options(device: int = -1, rewrite: bool = True, rng: str = "philox", jit="auto"):
+def _options(device: int = -1, rewrite: bool = True, rng: str = "philox", jit="auto",
+             devices: Sequence[int] | None = None, fault: bool = False):
     if rng not in RNG_MODES:
         raise ValueError(f"rng must be one of {sorted(RNG_MODES)}")
     if jit not in JIT_MODES:
@@ -216,6 +218,13 @@ def _options(device: int = -1, rewrite: bool = True, rng: str = "philox", jit="a
     o = _native.OptionsC()
     o.device, o.rewrite, o.rng = int(device), int(bool(rewrite)), RNG_MODES[rng]
     o.jit = JIT_MODES[jit]
+    devs = [int(d) for d in (devices or [])]
+    if len(devs) > _native.MAX_DEVICES:
+        raise ValueError(f"at most {_native.MAX_DEVICES} devices")
+    o.n_devices = len(devs)
+    for i, d in enumerate(devs):
+        o.devices[i] = d
+    o.fault_inject = int(bool(fault))
     return o
 
 
@@ -225,7 +234,8 @@ def version() -> str:
 
 def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, seed: int = 0,
           days: Sequence[int] = (0,), tenv: dict | None = None, threads: int = 0,
-          device: int = -1, rng: str = "philox", jit="auto") -> list[dict]:
+          device: int = -1, rng: str = "philox", jit="auto",
+          devices: Sequence[int] | None = None) -> list[dict]:
     """priceAcrossTime on the GPU (cltk.price, proj/python/bindings.cpp:103-126).
 
     Returns one dict per valuation day: ``price``, ``std_error``, ``paths``,
@@ -235,16 +245,19 @@ def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, s
     (Sobol + AS241 + Brownian bridge).  ``jit``: ``"auto"`` (default) evaluates
     the payoff with the NVRTC-generated kernel when NVRTC is available (compiled
     once per program shape and cached in-process and on disk), ``True`` always,
-    ``False`` with the bytecode interpreter -- bit-identical results."""
+    ``False`` with the bytecode interpreter -- bit-identical results.
+    ``devices``: shard the call over these GPUs of this process (one NCCL
+    all-gather of the chunk partials; bit-identical to one GPU); default: the
+    GPUs ``$CLTK_DEVICES`` lists, else ``device``."""
     L = _native.lib()
     d, nd = _days(days)
     out = (_native.PriceResultC * max(1, nd))()
     err = _native.ErrorC()
-    if rng == "philox" and jit == "auto":
+    if rng == "philox" and jit == "auto" and not devices:
         rc = L.cltk_gpu_price(_kernel_json(kernel), _model_json(model), int(paths), int(seed), d,
                               nd, _tenv_json(tenv), int(threads), int(device), out, C.byref(err))
     else:
-        o = _options(device, True, rng, jit)
+        o = _options(device, True, rng, jit, devices)
         rc = L.cltk_gpu_price_ex(_kernel_json(kernel), None, 1, 0, _model_json(model), int(paths),
                                  int(seed), d, nd, _tenv_json(tenv), C.byref(o), out,
                                  C.byref(err))
@@ -254,7 +267,8 @@ def price(kernel: Kernel | str | dict, model: str | dict, paths: int = 100000, s
 
 def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths: int = 100000,
                 seed: int = 0, days: Sequence[int] = (0,), tenv: dict | None = None,
-                device: int = -1, rng: str = "philox", jit="auto") -> list[list[dict]]:
+                device: int = -1, rng: str = "philox", jit="auto",
+                devices: Sequence[int] | None = None) -> list[list[dict]]:
     """Price literal instances of one template on one shared path set (no
     recompilation per instance): ``[instance][day]`` result dicts."""
     L = _native.lib()
@@ -263,11 +277,11 @@ def price_batch(kernels: Sequence[Kernel | str | dict], model: str | dict, paths
     arr = (C.c_char_p * n)(*[_kernel_json(k) for k in kernels])
     out = (_native.PriceResultC * max(1, n * nd))()
     err = _native.ErrorC()
-    if rng == "philox" and jit == "auto":
+    if rng == "philox" and jit == "auto" and not devices:
         rc = L.cltk_gpu_price_batch(arr, n, _model_json(model), int(paths), int(seed), d, nd,
                                     _tenv_json(tenv), int(device), out, C.byref(err))
     else:
-        o = _options(device, True, rng, jit)
+        o = _options(device, True, rng, jit, devices)
         rc = L.cltk_gpu_price_batch_ex(arr, n, _model_json(model), int(paths), int(seed), d, nd,
                                        _tenv_json(tenv), C.byref(o), out, C.byref(err))
     _raise(rc, err)
@@ -291,7 +305,8 @@ def kernel_literals(kernel: Kernel | str | dict) -> list[float]:
 def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
                    paths: int = 100000, seed: int = 0, days: Sequence[int] = (0,),
                    tenv: dict | None = None, device: int = -1,
-                   rng: str = "philox", jit="auto") -> list[list[dict]]:
+                   rng: str = "philox", jit="auto",
+                   devices: Sequence[int] | None = None) -> list[list[dict]]:
     """Price instances of one template given as a literal table
     ``literals[instance][j]`` (j in ``kernel_literals`` order): one compile,
     one path set, the literals passed to the kernel as data."""
@@ -304,7 +319,7 @@ def price_template(kernel: Kernel | str | dict, literals, model: str | dict,
     n = lit.shape[0]
     out = (_native.PriceResultC * max(1, n * nd))()
     err = _native.ErrorC()
-    o = _options(device, True, rng, jit)
+    o = _options(device, True, rng, jit, devices)
     rc = L.cltk_gpu_price_ex(_kernel_json(kernel), lit.ctypes.data, n, lit.shape[1],
                              _model_json(model), int(paths), int(seed), d, nd, _tenv_json(tenv),
                              C.byref(o), out, C.byref(err))
@@ -395,7 +410,10 @@ class Plan:
 
     def __init__(self, kernels: Sequence[Kernel | str | dict] | Kernel, model: str | dict,
                  days: Sequence[int] = (0,), tenv: dict | None = None, device: int = -1,
-                 rewrite: bool = True, literals=None, rng: str = "philox", jit=False):
+                 rewrite: bool = True, literals=None, rng: str = "philox", jit=False,
+                 fault: bool = False):
+        """``fault=True`` (tests): the kernel with the fault hook compiled in
+        (``set_fault``)."""
         if not isinstance(kernels, (list, tuple)):
             kernels = [kernels]
         self._L = _native.lib()
@@ -405,7 +423,7 @@ class Plan:
         err = _native.ErrorC()
         if literals is not None:
             import numpy as np
-            o = _options(device, rewrite, rng, jit)
+            o = _options(device, rewrite, rng, jit, fault=fault)
             lit = np.ascontiguousarray(literals, dtype=np.float64)
             lp, n_i, n_l = lit.ctypes.data, lit.shape[0], lit.shape[1]
             if len(kernels) != 1:
@@ -415,7 +433,7 @@ class Plan:
                 _tenv_json(tenv), C.byref(o), C.byref(self._h), C.byref(err))
         else:
             arr = (C.c_char_p * len(kernels))(*[_kernel_json(k) for k in kernels])
-            o = _options(device, rewrite, rng, jit)
+            o = _options(device, rewrite, rng, jit, fault=fault)
             rc = self._L.cltk_plan_create_batch_ex(arr, len(kernels), _model_json(model), d, nd,
                                                    _tenv_json(tenv), C.byref(o),
                                                    C.byref(self._h), C.byref(err))
@@ -461,6 +479,14 @@ class Plan:
                                         d, nd, C.c_void_p(stream_ptr), out, C.byref(err))
         _raise(rc, err)
         return _results(out, n)
+
+    def set_fault(self, path: int, draw: int) -> None:
+        """Test hook (plans built with ``fault=True``): later launches force
+        the uniform of ``draw`` of ``path`` to exactly 1.0 -- the reference's
+        invNormalCdf domain error.  ``path=-1``: none."""
+        err = _native.ErrorC()
+        rc = self._L.cltk_plan_set_fault(self._h, int(path) & (2**64 - 1), int(draw), C.byref(err))
+        _raise(rc, err)
 
     def error_word(self, stream_ptr: int = 0) -> int:
         w = C.c_uint64()
@@ -530,6 +556,28 @@ def debug_math(fn: str, x, device: int = -1):
                                        C.byref(err))
     _raise(rc, err)
     return out
+
+
+def debug_sobol(n0: int, n: int, d0: int, nd: int, aligned: bool = True, device: int = -1):
+    """Sobol integers [n][nd] of points n0.. and dimensions d0.. from the
+    device generator of the QMC mode (``aligned``: its warp-cooperative
+    skip-ahead, n0 % 32 == 0)."""
+    import numpy as np
+    out = np.zeros((n, nd), dtype=np.uint32)
+    err = _native.ErrorC()
+    rc = _native.lib().cltk_debug_sobol(int(device), int(n0), int(n), int(d0), int(nd),
+                                        int(bool(aligned)), out.ctypes.data, C.byref(err))
+    _raise(rc, err)
+    return out
+
+
+def nccl_version() -> int:
+    """NCCL version code the in-process multi-GPU path loads (raises
+    ContractUnsupportedError when libnccl.so.2 is not loadable)."""
+    v = C.c_int()
+    err = _native.ErrorC()
+    _raise(_native.lib().cltk_nccl_version(C.byref(v), C.byref(err)), err)
+    return v.value
 
 
 def fp64_peak(device: int = -1, iters: int = 4096) -> tuple[float, float]:

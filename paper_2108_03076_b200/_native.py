@@ -21,13 +21,18 @@ EXPORTS = [
     "cltk_fp64_peak", "cltk_black_scholes_call", "cltk_gpu_price_template",
     "cltk_kernel_literals", "cltk_plan_create_template", "cltk_gpu_price_ex",
     "cltk_plan_create_ex", "cltk_jit_source", "cltk_jit_compile", "cltk_reindex",
-    "cltk_plan_create_batch_ex", "cltk_gpu_price_batch_ex",
+    "cltk_plan_create_batch_ex", "cltk_gpu_price_batch_ex", "cltk_plan_set_fault",
+    "cltk_nccl_version", "cltk_debug_sobol",
 ]
+
+
+MAX_DEVICES = 16  # CLTK_MAX_DEVICES
 
 
 class OptionsC(C.Structure):
     _fields_ = [("device", C.c_int), ("rewrite", C.c_int), ("rng", C.c_int), ("jit", C.c_int),
-                ("reserved", C.c_int * 4)]
+                ("n_devices", C.c_int), ("devices", C.c_int * MAX_DEVICES),
+                ("fault_inject", C.c_int), ("reserved", C.c_int * 3)]
 
 
 class PriceResultC(C.Structure):
@@ -125,6 +130,12 @@ def lib() -> C.CDLL:
     L.cltk_debug_rng.argtypes = [i32, u64, u64, u64, u64, vp, vp, vp, PE]
     L.cltk_debug_math.restype = i32
     L.cltk_debug_math.argtypes = [i32, i32, vp, u64, vp, PE]
+    L.cltk_plan_set_fault.restype = i32
+    L.cltk_plan_set_fault.argtypes = [vp, u64, u32, PE]
+    L.cltk_nccl_version.restype = i32
+    L.cltk_nccl_version.argtypes = [C.POINTER(i32), PE]
+    L.cltk_debug_sobol.restype = i32
+    L.cltk_debug_sobol.argtypes = [i32, u64, u64, u32, u32, i32, vp, PE]
     L.cltk_fp64_peak.restype = i32
     L.cltk_fp64_peak.argtypes = [i32, i32, PD, PD, PE]
     L.cltk_black_scholes_call.restype = dbl

@@ -11,6 +11,7 @@
 #include "compiler.hpp"
 #include "jit.hpp"
 #include "engine_launch.hpp"
+#include "nccl_comm.hpp"
 
 using namespace cltk::b200;
 
@@ -80,6 +81,11 @@ int resolvedDevice(int device) {
   cudaGetDevice(&d);
   return d;
 }
+std::vector<int> resolvedDevices(const RunOptions& opt) {
+  std::vector<int> v = resolveDevices(opt);
+  for (int& d : v) d = resolvedDevice(d);
+  return v;
+}
 }  // namespace
 
 extern "C" {
@@ -108,15 +114,16 @@ int cltk_gpu_price(const char* kernel_json, const char* model_json, uint64_t pat
     kb.str(model_json);
     kb.str(tenv_json);
     kb.add(d.data(), d.size() * sizeof(uint64_t));
-    kb.val(resolvedDevice(device));
     auto r = priceCached(
         kb.key,
-        [&] {
+        [&](int dev) {
           const Kernel k = kernelFromWire(kernel_json);
+          RunOptions o = opt;
+          o.device = resolvedDevice(dev);
           return std::make_unique<Plan>(std::vector<const Kernel*>{&k},
-                                        modelFromJson(model_json), d, tenvOf(tenv_json), opt);
+                                        modelFromJson(model_json), d, tenvOf(tenv_json), o);
         },
-        paths, seed, d);
+        resolvedDevices(opt), paths, seed, d);
     toC(r, results);
   });
 }
@@ -192,6 +199,12 @@ RunOptions optionsOf(const cltk_options* o) {
     r.rewrite = o->rewrite != 0;
     r.rng = o->rng;
     r.jit = o->jit;
+    if (o->n_devices < 0 || o->n_devices > CLTK_MAX_DEVICES)
+      throw UnsupportedError("cltk_options: n_devices out of range");
+    r.devices.assign(o->devices, o->devices + o->n_devices);
+    for (int d : r.devices)
+      if (d < 0) throw UnsupportedError("cltk_options: negative device id");
+    r.faultInject = o->fault_inject != 0;
   }
   return r;
 }
@@ -211,7 +224,6 @@ int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_
     kb.str(model_json);
     kb.str(tenv_json);
     kb.add(d.data(), d.size() * sizeof(uint64_t));
-    kb.val(resolvedDevice(opt.device));
     kb.val(opt.rewrite);
     kb.val(opt.rng);
     kb.val(opt.jit);
@@ -220,7 +232,9 @@ int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_
     if (literals) kb.add(literals, n_instances * n_literals * sizeof(double));
     auto r = priceCached(
         kb.key,
-        [&] {
+        [&](int dev) {
+          RunOptions o = opt;
+          o.device = dev;
           const Kernel k = kernelFromWire(kernel_json);
           std::vector<double> own;
           const double* lit = literals;
@@ -232,9 +246,9 @@ int cltk_gpu_price_ex(const char* kernel_json, const double* literals, size_t n_
             nl = own.size();
           }
           return std::make_unique<Plan>(k, lit, ni, nl, modelFromJson(model_json), d,
-                                        tenvOf(tenv_json), opt);
+                                        tenvOf(tenv_json), o);
         },
-        paths, seed, d);
+        resolvedDevices(opt), paths, seed, d);
     toC(r, results);
   });
 }
@@ -346,6 +360,23 @@ int cltk_plan_finalize(cltk_plan* plan, uint64_t paths, uint64_t seed, const voi
       for (std::size_t i = 0; i < r.size(); ++i) r[i].valuationDay = days[i % n_days];
     toC(r, results);
   });
+}
+
+int cltk_plan_set_fault(cltk_plan* plan, uint64_t path, uint32_t draw, cltk_error* err) {
+  return guarded(err, [&] { plan->plan->setFault(path, draw); });
+}
+
+int cltk_nccl_version(int* version, cltk_error* err) {
+  return guarded(err, [&] {
+    std::string info;
+    if (!ncclAvailable(&info)) throw UnsupportedError("multi-GPU: " + info);
+    *version = std::atoi(info.c_str() + 5);  // "nccl <code>"
+  });
+}
+
+int cltk_debug_sobol(int device, uint64_t n0, uint64_t n, uint32_t d0, uint32_t nd, int aligned,
+                     uint32_t* out, cltk_error* err) {
+  return guarded(err, [&] { debugSobol(device, n0, n, d0, nd, aligned != 0, out); });
 }
 
 int cltk_plan_error_word(cltk_plan* plan, void* stream, uint64_t* word) {

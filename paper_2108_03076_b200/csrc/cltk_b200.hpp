@@ -159,6 +159,16 @@ struct RunOptions {
   // (default: the one-shot entry points price with the generated kernel,
   // compiled once per program shape and cached in-process and on disk).
   int jit = 2;
+  // One-shot pricing over several GPUs of this process: the plan is built on
+  // every listed device, the deterministic chunks are sharded in contiguous
+  // equal slices, one NCCL all-gather assembles the chunk partials, and the
+  // fixed-order combine runs on the first device -- results bit-identical to
+  // one device.  Empty: the single `device`.  A device may repeat (tests:
+  // the shards then share one GPU and are gathered with device copies).
+  std::vector<int> devices;
+  // Test build: the path kernel with the RunArgs fault hook compiled in
+  // (Plan::setFault); never set on the pricing path.
+  bool faultInject = false;
 };
 
 // ---- compiled plan (host + device state) ------------------------------------
@@ -200,6 +210,11 @@ class Plan {
   std::vector<PriceResult> finalize(uint64_t paths, uint64_t seed, const void* partialsDev,
                                     void* stream);
   std::string dump() const;  // program listing (JSON) for tests / DESIGN.md
+  // Test hook (plans built with RunOptions::faultInject): later launches
+  // force the uniform of draw `draw` of path `path` to exactly 1.0, the
+  // reference's invNormalCdf domain error (path = ~0: none).
+  void setFault(uint64_t path, uint32_t draw);
+  int device() const;
   PlanImpl* impl() { return impl_.get(); }
 
  private:
@@ -217,6 +232,10 @@ uint64_t debugPaths(Plan& plan, uint64_t seed, uint64_t path0, uint64_t npaths, 
 void debugRng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n, uint64_t* bits,
               double* uniforms, double* normals);
 double fp64Peak(int device, int iters, double* seconds);
+// Sobol integers of points [n0, n0+n), dims [d0, d0+nd) from the device
+// generator (out[n][nd], host buffer).
+void debugSobol(int device, uint64_t n0, uint64_t n, uint32_t d0, uint32_t nd, bool aligned,
+                uint32_t* out);
 // Device exp / log / erfc / invNormalCdf (fn 0..3) over a host array.
 void debugMath(int device, int fn, const double* x, uint64_t n, double* out);
 
@@ -238,10 +257,15 @@ std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* litera
 // keyed by the caller's exact wire inputs, options and device): a repeated
 // call skips parsing, compiling and uploading.  make() builds the plan on a
 // miss.  Plans in the cache are used by one caller at a time.
+// make(device) builds the plan on one device; with several devices the call
+// is sharded over them (RunOptions::devices).
 std::vector<PriceResult> priceCached(const std::string& key,
-                                     const std::function<std::unique_ptr<Plan>()>& make,
-                                     uint64_t paths, uint64_t seed,
-                                     const std::vector<uint64_t>& days);
+                                     const std::function<std::unique_ptr<Plan>(int)>& make,
+                                     const std::vector<int>& devices, uint64_t paths,
+                                     uint64_t seed, const std::vector<uint64_t>& days);
+// The devices a one-shot call with these options runs on: opt.devices, else
+// $CLTK_DEVICES ("all" or "0,1,...") when opt.device < 0, else {opt.device}.
+std::vector<int> resolveDevices(const RunOptions& opt);
 // Template batch: instances share one path set (common random numbers, like
 // repeated reference calls with one seed); result [instance * days + d].
 std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,

@@ -66,6 +66,7 @@ struct CompiledProgram {
   uint64_t kernelNodes = 0, dagNodes = 0;
   uint32_t nSharedOps = 0, nInstOps = 0;
   std::string listing;                 // JSON dump
+  bool faultBuild = false;             // test build: RunArgs fault injection compiled in
 };
 
 struct CompileOptions {

@@ -18,6 +18,7 @@
 #include "compiler.hpp"
 #include "engine_launch.hpp"
 #include "jit.hpp"
+#include "nccl_comm.hpp"
 
 namespace cltk {
 namespace b200 {
@@ -107,6 +108,9 @@ struct PlanImpl {
   const void* jitFn = nullptr;  // NVRTC kernel (cudaKernel_t) or null: interpreter
   uint64_t drawsPerPath = 0;    // normals per path (chunk sizing)
   uint32_t pathBatch = 1;       // paths per normal batch (ppt is a multiple of it)
+  bool fault = false;           // test build (RunArgs fault hook compiled in)
+  uint64_t faultPath = ~0ULL;
+  uint32_t faultDraw = 0;
 
   ~PlanImpl() {
     int cur = 0;
@@ -176,13 +180,49 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
                     ? pathBatch(I.prog.header.n_steps * std::max<uint32_t>(1, I.prog.header.n_assets))
                     : 1;
   if (opt.jit < 0 || opt.jit > 2) throw UnsupportedError("unknown jit mode");
+  if (opt.faultInject && I.prog.header.rng != CLTK_RNG_PHILOX)
+    throw UnsupportedError("fault injection: Philox mode only");
+  I.fault = opt.faultInject;
+  I.prog.faultBuild = opt.faultInject;
   std::string jitSrc;
+  // jitSource rewrites the header's register window and the steps' classes:
+  // JIT_AUTO keeps the interpreter's copy in case NVRTC or the module load fails
+  std::vector<cltk_step> interpSteps;
+  cltk_plan_header interpHdr{};
   if (opt.jit != JIT_OFF) {
     std::string why;
     bool use = jitAvailable(&why);
     if (use && opt.jit == JIT_AUTO && jitOpCount(I.prog) > kJitAutoMaxOps) use = false;
     if (!use && opt.jit == JIT_ON) throw UnsupportedError("jit: " + why);
-    if (use) jitSrc = jitSource(I.prog);  // assigns steps[].jit_class (uploaded below)
+    if (use) {
+      interpSteps = I.prog.steps;
+      interpHdr = I.prog.header;
+      try {
+        jitSrc = jitSource(I.prog);  // assigns steps[].jit_class (uploaded below)
+      } catch (const Error&) {
+        if (opt.jit == JIT_ON) throw;
+        jitSrc.clear();
+        I.prog.steps = interpSteps;
+        I.prog.header = interpHdr;
+      }
+    }
+  }
+  int dev0 = opt.device;
+  if (dev0 < 0) ck(cudaGetDevice(&dev0), "cudaGetDevice");
+  if (!jitSrc.empty()) {
+    // build (or load) the module before the upload; under JIT_AUTO a failure
+    // (NVRTC compile error, module load) falls back to the interpreter
+    PlanImpl::DeviceGuard g0(dev0);
+    try {
+      I.jitFn = jitKernel(jitSrc);
+    } catch (const Error&) {
+      if (opt.jit == JIT_ON) throw;
+      cudaGetLastError();
+      jitSrc.clear();
+      I.jitFn = nullptr;
+      I.prog.steps = interpSteps;
+      I.prog.header = interpHdr;
+    }
   }
 
   int dev = opt.device;
@@ -224,8 +264,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   if (I.smem > 227 * 1024)
     throw UnsupportedError("compiled payoff needs " + std::to_string(I.smem) +
                            " bytes of shared memory per CTA (max 232448)");
-  if (!jitSrc.empty()) {
-    I.jitFn = jitKernel(jitSrc);
+  if (I.jitFn) {
     ck(cudaFuncSetAttribute(I.jitFn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
        "jit cudaFuncSetAttribute");
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&I.blocksPerSm, I.jitFn, kBlock, I.smem),
@@ -313,6 +352,8 @@ void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void*
   if (paths == 0) throw EvalError("path count must be positive");
   if (impl_->prog.header.rng == CLTK_RNG_SOBOL && paths > (1ULL << 32))
     throw UnsupportedError("Sobol mode: at most 2^32 paths (32-bit Sobol points)");
+  // the device error word is path << 24 | site (engine_device.cuh)
+  if (paths > (1ULL << 40)) throw UnsupportedError("at most 2^40 paths per call");
   PlanImpl& I = *impl_;
   PlanImpl::DeviceGuard g(I.device);
   uint64_t chunkPaths, nChunks;
@@ -345,12 +386,14 @@ void Plan::launch(uint64_t paths, uint64_t seed, uint64_t c0, uint64_t c1, void*
   a.errKey = I.errKey;
   a.chunkCounter = I.chunkCounter;
   a.accScratch = I.accScratch;
+  a.faultPath = I.fault ? I.faultPath : ~0ULL;
+  a.faultDraw = I.faultDraw;
   if (I.jitFn) {
     int accInSmem = I.accInSmem ? 1 : 0;
     void* args[] = {&I.dev, &a, &accInSmem};
     ck(cudaLaunchKernel(I.jitFn, dim3(grid), dim3(kBlock), args, I.smem, s), "jit path kernel launch");
   } else {
-    ck(launchPath(I.dev, a, grid, I.smem, s), "path kernel launch");
+    ck(launchPath(I.dev, a, grid, I.smem, s, I.fault), "path kernel launch");
   }
 }
 
@@ -401,6 +444,14 @@ std::vector<PriceResult> Plan::finalize(uint64_t paths, uint64_t seed, const voi
 }
 
 std::string Plan::dump() const { return impl_->prog.listing; }
+
+void Plan::setFault(uint64_t path, uint32_t draw) {
+  if (!impl_->fault) throw UnsupportedError("fault injection: plan not built with fault_inject");
+  impl_->faultPath = path;
+  impl_->faultDraw = draw;
+}
+
+int Plan::device() const { return impl_->device; }
 
 uint64_t planErrorWord(Plan& plan, void* stream) {
   PlanImpl& I = *plan.impl();
@@ -485,6 +536,35 @@ void debugMath(int device, int fn, const double* x, uint64_t n, double* out) {
   cudaFree(dy);
 }
 
+void debugSobol(int device, uint64_t n0, uint64_t n, uint32_t d0, uint32_t nd, bool aligned,
+                uint32_t* out) {
+  if (static_cast<uint64_t>(d0) + nd > kSobolDims)
+    throw UnsupportedError("debug_sobol: dimensions beyond the direction-number table");
+  if (aligned && (n0 % 32) != 0) throw UnsupportedError("debug_sobol: aligned needs n0 % 32 == 0");
+  if (n == 0 || nd == 0) return;
+  if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+  std::vector<uint32_t> V(kSobolV, kSobolV + kSobolDims * 32), T5(kSobolDims * 32);
+  for (uint32_t d = 0; d < kSobolDims; ++d)  // the table Plan::init uploads
+    for (uint32_t g = 0; g < 32; ++g) {
+      uint32_t x = 0;
+      for (uint32_t k = 0; k < 5; ++k)
+        if ((g >> k) & 1u) x ^= V[d * 32 + k];
+      T5[d * 32 + g] = x;
+    }
+  uint32_t *dV = nullptr, *dT = nullptr, *dO = nullptr;
+  ck(cudaMalloc(&dV, V.size() * 4), "cudaMalloc");
+  ck(cudaMalloc(&dT, T5.size() * 4), "cudaMalloc");
+  ck(cudaMalloc(&dO, n * nd * 4), "cudaMalloc");
+  ck(cudaMemcpy(dV, V.data(), V.size() * 4, cudaMemcpyHostToDevice), "H2D");
+  ck(cudaMemcpy(dT, T5.data(), T5.size() * 4, cudaMemcpyHostToDevice), "H2D");
+  ck(launchSobolDump(dV, dT, n0, n, d0, nd, aligned, dO, nullptr), "sobol launch");
+  ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  ck(cudaMemcpy(out, dO, n * nd * 4, cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(dV);
+  cudaFree(dT);
+  cudaFree(dO);
+}
+
 double fp64Peak(int device, int iters, double* seconds) {
   if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
   int dev = 0, sms = 0;
@@ -511,44 +591,151 @@ double fp64Peak(int device, int iters, double* seconds) {
   return flops / (ms * 1e-3) / 1e12;
 }
 
-// ---- one-shot pricing on the plan's own buffers ----------------------------
+// ---- one-shot pricing on the plans' own buffers -----------------------------
+std::vector<int> resolveDevices(const RunOptions& opt) {
+  if (!opt.devices.empty()) return opt.devices;
+  if (opt.device < 0) {
+    // CLTK_DEVICES: "all" or a comma-separated list shards every one-shot call
+    // whose caller did not name a device (the C++ priceAcrossTime, cltk_gpu_price)
+    if (const char* env = std::getenv("CLTK_DEVICES"); env && *env) {
+      std::vector<int> v;
+      if (std::strcmp(env, "all") == 0) {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        for (int d = 0; d < n; ++d) v.push_back(d);
+      } else {
+        for (const char* q = env; *q;) {
+          char* e = nullptr;
+          const long d = std::strtol(q, &e, 10);
+          if (e == q || d < 0) throw UnsupportedError(std::string("CLTK_DEVICES: bad list ") + env);
+          v.push_back(static_cast<int>(d));
+          q = *e == ',' ? e + 1 : e;
+          if (*e && *e != ',') throw UnsupportedError(std::string("CLTK_DEVICES: bad list ") + env);
+        }
+      }
+      if (!v.empty()) return v;
+    }
+  }
+  return {opt.device};
+}
+
 namespace {
 
-std::vector<PriceResult> runOnce(Plan& plan, uint64_t paths, uint64_t seed,
-                                 const std::vector<uint64_t>& days) {
-  PlanImpl& I = *plan.impl();
+cltk_partial* ownPartials(PlanImpl& I, uint64_t nChunks) {
   PlanImpl::DeviceGuard g(I.device);
-  uint64_t chunkPaths, nChunks;
-  plan.chunking(paths, &chunkPaths, &nChunks);
   if (nChunks > I.ownPartialsChunks) {
     devFree(I.ownPartials);
     I.ownPartials = static_cast<cltk_partial*>(
         devMalloc(nChunks * std::max<uint32_t>(1, I.nOut) * sizeof(cltk_partial)));
     I.ownPartialsChunks = nChunks;
   }
-  cudaStream_t s = nullptr;
-  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-  std::vector<PriceResult> r;
-  try {
-    plan.launch(paths, seed, 0, nChunks, I.ownPartials, s);
-    r = plan.finalize(paths, seed, I.ownPartials, s);
-  } catch (...) {
-    cudaStreamDestroy(s);
-    throw;
+  return I.ownPartials;
+}
+
+struct Streams {
+  std::vector<cudaStream_t> s;
+  std::vector<int> dev;
+  ~Streams() {
+    for (size_t g = 0; g < s.size(); ++g) {
+      cudaSetDevice(dev[g]);
+      cudaStreamDestroy(s[g]);
+    }
   }
-  cudaStreamDestroy(s);
+};
+
+// The reference's runParallel (proj/src/pricing.cpp:268-286, 345-364) across
+// the GPUs of this process: plan g prices the contiguous chunk slice
+// [g S, min(C, (g+1) S)), S = ceil(C / G), into its own full-size partials
+// buffer; ONE in-place NCCL all-gather over NVLink assembles every buffer
+// (distinct devices), or device copies into plan 0's buffer (a device listed
+// twice: tests on one GPU); the device error words merge by MIN (the lowest
+// failing path wins, as on one GPU) and plan 0 runs the fixed-order combine.
+// Chunking depends only on (paths, outputs): bit-identical for any G.
+std::vector<PriceResult> runGroup(const std::vector<Plan*>& plans, uint64_t paths, uint64_t seed,
+                                  const std::vector<uint64_t>& days) {
+  static const bool trace = std::getenv("CLTK_TRACE") != nullptr;
+  const size_t G = plans.size();
+  uint64_t chunkPaths, nChunks;
+  plans[0]->chunking(paths, &chunkPaths, &nChunks);
+  const uint64_t S = (nChunks + G - 1) / G;
+  const uint32_t nOut = std::max<uint32_t>(1, plans[0]->impl()->nOut);
+  Streams st;
+  std::vector<double*> bufs(G);
+  std::vector<int> devs(G);
+  for (size_t g = 0; g < G; ++g) {
+    PlanImpl& I = *plans[g]->impl();
+    devs[g] = I.device;
+    bufs[g] = reinterpret_cast<double*>(ownPartials(I, G == 1 ? nChunks : G * S));
+    PlanImpl::DeviceGuard dg(I.device);
+    cudaStream_t s = nullptr;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    st.s.push_back(s);
+    st.dev.push_back(I.device);
+  }
+  for (size_t g = 0; g < G; ++g)  // asynchronous: the devices run concurrently
+    plans[g]->launch(paths, seed, G == 1 ? 0 : g * S, G == 1 ? nChunks : std::min(nChunks, (g + 1) * S),
+                     bufs[g], st.s[g]);
+  if (G > 1) {
+    bool distinct = true;
+    for (size_t a = 0; a < G; ++a)
+      for (size_t b = a + 1; b < G; ++b) distinct = distinct && devs[a] != devs[b];
+    std::string why;
+    const size_t slice = static_cast<size_t>(S) * nOut * (sizeof(cltk_partial) / sizeof(double));
+    if (distinct && ncclAvailable(&why)) {
+      ncclAllGatherInPlace(*ncclClique(devs), bufs, slice, st.s);
+      if (trace) std::fprintf(stderr, "[cltk] %zu GPUs: NCCL all-gather (%s), %zu B per rank\n",
+                              G, why.c_str(), slice * sizeof(double));
+    } else {
+      if (distinct) throw UnsupportedError("multi-GPU: " + why);
+      PlanImpl::DeviceGuard dg(devs[0]);
+      for (size_t g = 1; g < G; ++g) {
+        const uint64_t c0 = g * S, c1 = std::min(nChunks, (g + 1) * S);
+        if (c0 >= c1) continue;
+        cudaEvent_t ev;
+        {
+          PlanImpl::DeviceGuard dgg(devs[g]);
+          ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+          ck(cudaEventRecord(ev, st.s[g]), "cudaEventRecord");
+        }
+        ck(cudaStreamWaitEvent(st.s[0], ev, 0), "cudaStreamWaitEvent");
+        ck(cudaMemcpyPeerAsync(bufs[0] + c0 * nOut * 3, devs[0], bufs[g] + c0 * nOut * 3, devs[g],
+                               (c1 - c0) * nOut * sizeof(cltk_partial), st.s[0]),
+           "cudaMemcpyPeerAsync");
+        cudaEventDestroy(ev);
+      }
+    }
+    // error words: MIN over the shards, the other plans' words reset
+    uint64_t w = ~0ULL;
+    for (size_t g = 0; g < G; ++g) w = std::min<uint64_t>(w, planErrorWord(*plans[g], st.s[g]));
+    for (size_t g = 1; g < G; ++g) planSetErrorWord(*plans[g], st.s[g], ~0ULL);
+    planSetErrorWord(*plans[0], st.s[0], w);
+  }
+  std::vector<PriceResult> r = plans[0]->finalize(paths, seed, bufs[0], st.s[0]);
   const uint32_t nd = static_cast<uint32_t>(days.size());
   for (std::size_t i = 0; i < r.size(); ++i) r[i].valuationDay = days[i % nd];
   return r;
 }
 
-}  // namespace
+using PlanGroup = std::vector<std::unique_ptr<Plan>>;
 
-namespace {
-// A one-shot call: plan, run on its own buffers, free.  CLTK_TRACE=1 prints
+PlanGroup makeGroup(const std::function<std::unique_ptr<Plan>(int)>& make,
+                    const std::vector<int>& devices) {
+  PlanGroup g;
+  for (int d : devices) g.push_back(make(d));
+  return g;
+}
+
+std::vector<PriceResult> runGroup(PlanGroup& g, uint64_t paths, uint64_t seed,
+                                  const std::vector<uint64_t>& days) {
+  std::vector<Plan*> p;
+  for (auto& x : g) p.push_back(x.get());
+  return runGroup(p, paths, seed, days);
+}
+
+// A one-shot call: plans, run on their own buffers, free.  CLTK_TRACE=1 prints
 // where the host time goes (stderr).
-template <class MakePlan>
-std::vector<PriceResult> oneShot(MakePlan make, uint64_t paths, uint64_t seed,
+std::vector<PriceResult> oneShot(const std::function<std::unique_ptr<Plan>(int)>& make,
+                                 const std::vector<int>& devices, uint64_t paths, uint64_t seed,
                                  const std::vector<uint64_t>& days) {
   static const bool trace = std::getenv("CLTK_TRACE") != nullptr;
   using clk = std::chrono::steady_clock;
@@ -556,10 +743,10 @@ std::vector<PriceResult> oneShot(MakePlan make, uint64_t paths, uint64_t seed,
   std::vector<PriceResult> r;
   double tPlan = 0.0, tRun = 0.0;
   {
-    std::unique_ptr<Plan> plan = make();
+    PlanGroup g = makeGroup(make, devices);
     if (days.empty()) return {};
     const auto t1 = clk::now();
-    r = runOnce(*plan, paths, seed, days);
+    r = runGroup(g, paths, seed, days);
     tPlan = std::chrono::duration<double, std::milli>(t1 - t0).count();
     tRun = std::chrono::duration<double, std::milli>(clk::now() - t1).count();
   }
@@ -573,12 +760,12 @@ std::vector<PriceResult> oneShot(MakePlan make, uint64_t paths, uint64_t seed,
 }  // namespace
 
 std::vector<PriceResult> priceCached(const std::string& key,
-                                     const std::function<std::unique_ptr<Plan>()>& make,
-                                     uint64_t paths, uint64_t seed,
-                                     const std::vector<uint64_t>& days) {
+                                     const std::function<std::unique_ptr<Plan>(int)>& make,
+                                     const std::vector<int>& devices, uint64_t paths,
+                                     uint64_t seed, const std::vector<uint64_t>& days) {
   struct Entry {
     std::string key;
-    std::unique_ptr<Plan> plan;
+    PlanGroup plans;
     std::mutex use;
   };
   constexpr size_t kEntries = 4;
@@ -586,23 +773,22 @@ std::vector<PriceResult> priceCached(const std::string& key,
   static std::vector<std::shared_ptr<Entry>> lru;  // most recent last
   if (paths == 0) throw EvalError("path count must be positive");
   if (days.empty()) {  // nothing to price; the inputs are still validated
-    (void)make();
+    (void)makeGroup(make, devices);
     return {};
   }
-  // CLTK_PLAN_CACHE=0: every call builds (parses, compiles, uploads) its plan
+  // CLTK_PLAN_CACHE=0: every call builds (parses, compiles, uploads) its plans
   static const bool enabled = [] {
     const char* v = std::getenv("CLTK_PLAN_CACHE");
     return v == nullptr || std::strcmp(v, "0") != 0;
   }();
-  if (!enabled) {
-    std::unique_ptr<Plan> plan = make();
-    return runOnce(*plan, paths, seed, days);
-  }
+  if (!enabled) return oneShot(make, devices, paths, seed, days);
+  std::string k = key;
+  for (int d : devices) k.append(reinterpret_cast<const char*>(&d), sizeof d);
   std::shared_ptr<Entry> e;
   {
     std::lock_guard<std::mutex> lock(mu);
     for (size_t i = 0; i < lru.size(); ++i)
-      if (lru[i]->key == key) {
+      if (lru[i]->key == k) {
         e = lru[i];
         lru.erase(lru.begin() + static_cast<std::ptrdiff_t>(i));
         lru.push_back(e);
@@ -611,15 +797,15 @@ std::vector<PriceResult> priceCached(const std::string& key,
   }
   if (!e) {
     e = std::make_shared<Entry>();
-    e->key = key;
-    e->plan = make();
+    e->key = k;
+    e->plans = makeGroup(make, devices);
     std::lock_guard<std::mutex> lock(mu);
     lru.push_back(e);
     if (lru.size() > kEntries) lru.erase(lru.begin());
   }
   std::lock_guard<std::mutex> use(e->use);
   try {
-    return runOnce(*e->plan, paths, seed, days);
+    return runGroup(e->plans, paths, seed, days);
   } catch (...) {  // a plan that failed on the device is not reused
     std::lock_guard<std::mutex> lock(mu);
     for (size_t i = 0; i < lru.size(); ++i)
@@ -636,8 +822,13 @@ std::vector<PriceResult> priceBatch(const std::vector<const Kernel*>& instances,
                                     const std::vector<uint64_t>& days, const TEnv& tenv,
                                     const RunOptions& opt) {
   if (paths == 0) throw EvalError("path count must be positive");
-  return oneShot([&] { return std::make_unique<Plan>(instances, model, days, tenv, opt); }, paths,
-                 seed, days);
+  return oneShot(
+      [&](int d) {
+        RunOptions o = opt;
+        o.device = d;
+        return std::make_unique<Plan>(instances, model, days, tenv, o);
+      },
+      resolveDevices(opt), paths, seed, days);
 }
 
 std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* literals,
@@ -647,10 +838,12 @@ std::vector<PriceResult> priceTemplate(const Kernel& templ, const double* litera
                                        const RunOptions& opt) {
   if (paths == 0) throw EvalError("path count must be positive");
   return oneShot(
-      [&] {
-        return std::make_unique<Plan>(templ, literals, nInstances, nLits, model, days, tenv, opt);
+      [&](int d) {
+        RunOptions o = opt;
+        o.device = d;
+        return std::make_unique<Plan>(templ, literals, nInstances, nLits, model, days, tenv, o);
       },
-      paths, seed, days);
+      resolveDevices(opt), paths, seed, days);
 }
 
 std::vector<PriceResult> priceAcrossTime(const Kernel& k, const ModelSpec& model,

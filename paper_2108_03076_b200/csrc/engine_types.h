@@ -67,6 +67,10 @@ struct RunArgs {
   unsigned long long* errKey;       // min(path << 24 | site)
   unsigned long long* chunkCounter; // dynamic chunk scheduler
   double* accScratch;               // global accumulators when n_out is large
+  // test builds only (FAULT kernels, cltk_plan_set_fault): the draw whose
+  // uniform is forced to 1.0; ~0 = none
+  uint64_t faultPath;
+  uint32_t faultDraw;
 };
 
 // Dump modes (tests): per-path outputs instead of reduction.

@@ -10,6 +10,7 @@
 #include <unistd.h>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <map>
 #include <mutex>
 #include <set>
@@ -530,7 +531,8 @@ std::string jitSource(CompiledProgram& prog) {
         "cltk_jit_path(const cltk::b200::DevPlan P, const cltk::b200::RunArgs A, int accInSmem) {\n"
         "  cltk::b200::path_body<"
      << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false") << ", cltk::b200::JitPayoff, "
-     << pb << ", " << (pb > 1 ? slots : 0) << ">(P, A, accInSmem);\n}\n";
+     << pb << ", " << (pb > 1 ? slots : 0) << ", " << (prog.faultBuild ? "true" : "false")
+     << ">(P, A, accInSmem);\n}\n";
   // Shared-memory register columns: only the registers the generated code
   // stores or loads (JW / JR) or the outputs read; the rest live in locals.
   std::string src = os.str();
@@ -596,8 +598,9 @@ bool readFile(const std::string& path, std::vector<uint8_t>* out) {
 }
 void writeFileAtomic(const std::string& path, const std::vector<uint8_t>& data) {
   const std::string dir = path.substr(0, path.rfind('/'));
-  std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
-  if (std::system(mk.c_str()) != 0) return;
+  std::error_code ec;  // best effort: no shell, no exception
+  std::filesystem::create_directories(dir, ec);
+  if (ec) return;
   const std::string tmp = path + ".tmp" + std::to_string(static_cast<long>(getpid()));
   FILE* f = std::fopen(tmp.c_str(), "wb");
   if (!f) return;

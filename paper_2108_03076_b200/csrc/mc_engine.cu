@@ -11,17 +11,20 @@ namespace b200 {
 
 namespace {
 
-template <int NA, bool QMC>
+template <int NA, bool QMC, bool FAULT = false>
 cudaError_t launchPathT(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
                         cudaStream_t s, int accInSmem) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(path_kernel<NA, QMC>,
+  // (per device: the attribute is a property of the kernel on the current device)
+  static bool configured[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64 || !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(path_kernel<NA, QMC, FAULT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    configured = true;
+    if (dev < 64) configured[dev] = true;
   }
-  path_kernel<NA, QMC><<<grid, kBlock, smem, s>>>(p, a, accInSmem);
+  path_kernel<NA, QMC, FAULT><<<grid, kBlock, smem, s>>>(p, a, accInSmem);
   return cudaGetLastError();
 }
 
@@ -95,8 +98,14 @@ int pathKernelOccupancy(const cltk_plan_header& h, size_t smem) {
   CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return (occupancyT<NA, false>(smem)));
 }
 
-cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem, cudaStream_t s) {
+cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem, cudaStream_t s,
+                       bool fault) {
   const int accInSmem = accFitsSmem(p.hdr) ? 1 : 0;
+  if (fault) {  // test builds of the Philox kernels (cltk_plan_set_fault)
+    if (p.hdr.rng == CLTK_RNG_SOBOL) return cudaErrorInvalidValue;
+    CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
+                   return (launchPathT<NA, false, true>(p, a, grid, smem, s, accInSmem)));
+  }
   if (p.hdr.rng == CLTK_RNG_SOBOL)
     CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
                    return (launchPathT<NA, true>(p, a, grid, smem, s, accInSmem)));
@@ -131,6 +140,13 @@ cudaError_t launchRngDump(uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
                           double* uniform, double* normal, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((n + 255) / 256);
   rng_kernel<<<grid, 256, 0, s>>>(seed, path, i0, n, bits, uniform, normal);
+  return cudaGetLastError();
+}
+
+cudaError_t launchSobolDump(const uint32_t* V, const uint32_t* T5, uint64_t n0, uint64_t n,
+                            uint32_t d0, uint32_t nd, bool aligned, uint32_t* out, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+  sobol_kernel<<<grid, 256, 0, s>>>(V, T5, n0, n, d0, nd, aligned ? 1 : 0, out);
   return cudaGetLastError();
 }
 
