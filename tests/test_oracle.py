@@ -107,3 +107,22 @@ def test_reference_library_agrees_with_golden():
     k, m = load_kernel("european-call"), load_model("call")
     r = ref.price(k, m, 1000, 42, [0], threads=2)
     assert r[0]["price"] == float.fromhex(c["prices"][1]["price"][0])
+
+
+def test_restatement_pinned_on_the_first_brc_paths_of_the_big_fixture():
+    """The C restatement against the reference's 10k-path BRC fixture
+    (oracle/make_golden_big.py): ext checksums and payoffs of the first
+    paths, and the 100k-path reference price."""
+    from golden_util import ext_checksums
+    z = np.load(os.path.join(GOLD, "paths", "brc_10k.npz"))
+    k, m = load_kernel("brc"), load_model("three")
+    n = 300
+    ext = np.stack([ORACLE.simulate_path(k, m, 42, p) for p in range(n)])
+    assert np.array_equal(ext_checksums(ext), z["ext_checksum"][:n])
+    _, pay = ORACLE.price(k, m, n, 42, [0], threads=os.cpu_count() or 1, want_payoffs=True)
+    assert np.array_equal(pay[0], z["payoffs"][:n])
+    big = json.load(open(os.path.join(GOLD, "big.json")))
+    p = next(x for x in big["prices"] if x["name"] == "brc" and x["paths"] == 100_000)
+    r = ORACLE.price(k, m, 100_000, 42, [0], threads=os.cpu_count() or 1)[0]
+    assert r["price"] == float.fromhex(p["price"][0])
+    assert r["std_error"] == float.fromhex(p["std_error"][0])
