@@ -1198,6 +1198,15 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   h.n_bridge_ops = static_cast<uint32_t>(plan.bridge.size());
   std::memcpy(h.chol, plan.chol, sizeof h.chol);
   std::memcpy(h.logS0, plan.logS0, sizeof h.logS0);
+  {
+    // one output and short paths: per-thread register accumulation of the
+    // output in the path kernel (engine_device.cuh path_body); long paths
+    // keep those registers for the normal batches
+    uint64_t draws = 0;
+    for (const cltk_step& st : P.steps)
+      if (st.draws == STEP_DRAW) draws += nA;
+    h.reg_acc = (nInst * days.size() == 1 && draws <= kRegAccMaxDraws) ? 1u : 0u;
+  }
   P.kernelNodes = k.nodes.size();
   P.dagNodes = static_cast<uint64_t>(N);
   P.nSharedOps = endBegin;

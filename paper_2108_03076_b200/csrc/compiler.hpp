@@ -69,6 +69,10 @@ struct CompiledProgram {
   bool faultBuild = false;             // test build: RunArgs fault injection compiled in
 };
 
+// Paths of at most this many normal draws with one output accumulate the
+// output per thread in registers (cltk_plan_header::reg_acc).
+constexpr uint64_t kRegAccMaxDraws = 64;
+
 struct CompileOptions {
   bool rewrite = true;
 };

@@ -532,7 +532,7 @@ std::string jitSource(CompiledProgram& prog) {
         "  cltk::b200::path_body<"
      << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false") << ", cltk::b200::JitPayoff, "
      << pb << ", " << (pb > 1 ? slots : 0) << ", " << (prog.faultBuild ? "true" : "false")
-     << ">(P, A, accInSmem);\n}\n";
+     << ", " << (h.reg_acc ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
   // Shared-memory register columns: only the registers the generated code
   // stores or loads (JW / JR) or the outputs read; the rest live in locals.
   std::string src = os.str();

@@ -122,6 +122,8 @@ typedef struct {
                             // columns (the NVRTC kernel keeps the S-slots in registers)
   uint32_t reg_top;         // path kernel: operand slots [reg_base, reg_top) have columns
                             // (n_thread; the NVRTC kernel: only the registers it stores)
+  uint32_t reg_acc;         // path kernel: 1 = one output, short paths: per-thread register
+                            // accumulation of the output, one warp sum per chunk
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
