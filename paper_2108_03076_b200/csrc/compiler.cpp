@@ -1206,6 +1206,11 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
     for (const cltk_step& st : P.steps)
       if (st.draws == STEP_DRAW) draws += nA;
     h.reg_acc = (nInst * days.size() == 1 && draws <= kRegAccMaxDraws) ? 1u : 0u;
+    // short Philox paths: normal batches that run on into the next path
+    // (long paths lose less to their last, partial batch than the stream's
+    // per-step bookkeeping costs)
+    const uint64_t slots = static_cast<uint64_t>(nSteps) * std::max<uint32_t>(1, nA);
+    h.stream = (plan.rng == CLTK_RNG_PHILOX && slots <= kStreamMaxSlots) ? 1u : 0u;
   }
   P.kernelNodes = k.nodes.size();
   P.dagNodes = static_cast<uint64_t>(N);

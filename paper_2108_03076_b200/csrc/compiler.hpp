@@ -72,6 +72,9 @@ struct CompiledProgram {
 // Paths of at most this many normal draws with one output accumulate the
 // output per thread in registers (cltk_plan_header::reg_acc).
 constexpr uint64_t kRegAccMaxDraws = 64;
+// Philox paths of at most this many normal slots (steps x assets) stream
+// through full normal batches (cltk_plan_header::stream).
+constexpr uint64_t kStreamMaxSlots = 64;
 
 struct CompileOptions {
   bool rewrite = true;

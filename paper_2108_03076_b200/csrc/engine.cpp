@@ -107,7 +107,7 @@ struct PlanImpl {
   uint32_t nOut = 0;
   const void* jitFn = nullptr;  // NVRTC kernel (cudaKernel_t) or null: interpreter
   uint64_t drawsPerPath = 0;    // normals per path (chunk sizing)
-  uint32_t pathBatch = 1;       // paths per normal batch (ppt is a multiple of it)
+  uint32_t streamPeriod = 1;    // ppt is a multiple of it (engine_types.h streamPeriod)
   bool fault = false;           // test build (RunArgs fault hook compiled in)
   uint64_t faultPath = ~0ULL;
   uint32_t faultDraw = 0;
@@ -175,10 +175,11 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   if (static_cast<uint64_t>(I.prog.header.n_steps) * std::max<uint32_t>(1, I.prog.header.n_assets) >=
       (1ULL << 32))
     throw UnsupportedError("more than 2^32 normal draws per path");
-  // path batches (engine_types.h pathBatch): normal slots per path = steps x assets
-  I.pathBatch = I.prog.header.rng == CLTK_RNG_PHILOX
-                    ? pathBatch(I.prog.header.n_steps * std::max<uint32_t>(1, I.prog.header.n_assets))
-                    : 1;
+  // Philox normal streams (engine_types.h streamPeriod): slots per path = steps x assets
+  I.streamPeriod = I.prog.header.stream
+                       ? streamPeriod(I.prog.header.n_steps * std::max<uint32_t>(1, I.prog.header.n_assets),
+                                      I.prog.header.n_assets)
+                       : 1;
   if (opt.jit < 0 || opt.jit > 2) throw UnsupportedError("unknown jit mode");
   if (opt.faultInject && I.prog.header.rng != CLTK_RNG_PHILOX)
     throw UnsupportedError("fault injection: Philox mode only");
@@ -314,9 +315,9 @@ void Plan::chunking(uint64_t paths, uint64_t* chunkPaths, uint64_t* nChunks) con
   const uint64_t pptBalance = std::max<uint64_t>(1, paths / (kBlock * 8192ull));
   ppt = std::max<uint64_t>(ppt, std::min(pptWork, pptBalance));
   ppt = std::max<uint64_t>(1, ppt);
-  // whole path batches per thread (a function of the program: the interpreted
+  // whole stream periods per thread (a function of the program: the interpreted
   // and the generated kernel chunk alike, so their results stay bit-identical)
-  const uint64_t pb = impl_->pathBatch;
+  const uint64_t pb = impl_->streamPeriod;
   ppt = (ppt + pb - 1) / pb * pb;
   *chunkPaths = ppt * kBlock;
   *nChunks = (paths + *chunkPaths - 1) / *chunkPaths;

@@ -16,17 +16,30 @@ constexpr int kWarps = kBlock / 32;
 #ifndef CLTK_MAX_BATCH
 #define CLTK_MAX_BATCH 6
 #endif
-// Short paths (Philox mode, at most half a batch of draws per path): one
-// batch draws the normals of pathBatch consecutive paths of a thread, so the
-// batch's fixed costs (barriers, pooled passes) are shared.  A function of the
-// program only (draws = steps x assets, every step's slots counted).
 #if defined(__CUDACC__)
 #define CLTK_TYPES_HD __host__ __device__
 #else
 #define CLTK_TYPES_HD
 #endif
-CLTK_TYPES_HD inline constexpr uint32_t pathBatch(uint32_t draws) {
-  return (draws >= 1 && 2 * draws <= CLTK_MAX_BATCH) ? CLTK_MAX_BATCH / draws : 1;
+// Simulation steps per normal batch (nA draws each).
+CLTK_TYPES_HD inline constexpr int batchSteps(int na) {
+  return na >= CLTK_MAX_BATCH ? 1 : CLTK_MAX_BATCH / na;
+}
+// Philox mode streams a thread's paths through full batches of
+// batchSteps(nA) * nA slots (engine_device.cuh path_body); after this many
+// paths of `draws` slots the stream is back at a batch boundary.  The host
+// makes the paths per thread of a chunk a multiple of it (no batch runs past
+// the chunk's last path).
+CLTK_TYPES_HD inline constexpr uint32_t streamPeriod(uint32_t draws, uint32_t na) {
+  uint32_t a = static_cast<uint32_t>(batchSteps(na < 1 ? 1 : static_cast<int>(na))) * (na < 1 ? 1 : na);
+  const uint32_t m = a;
+  uint32_t b = draws < 1 ? 1 : draws;
+  while (b) {  // gcd(batch slots, draws)
+    const uint32_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return m / a;
 }
 
 // Philox2x64-10 key schedule key_r = seed + r * 0x9E3779B97F4A7C15.

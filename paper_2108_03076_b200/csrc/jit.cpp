@@ -489,9 +489,6 @@ std::string jitSource(CompiledProgram& prog) {
       g.noLog.insert(bad);
     }
   }
-  // path batches (engine_types.h): the same choice the plan's chunking makes
-  const uint32_t slots = h.n_steps * nA;
-  const uint32_t pb = h.rng == CLTK_RNG_PHILOX ? pathBatch(slots) : 1;
   std::ostringstream os;
   os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
         "#define CLTK_JIT 1\n"
@@ -531,8 +528,8 @@ std::string jitSource(CompiledProgram& prog) {
         "cltk_jit_path(const cltk::b200::DevPlan P, const cltk::b200::RunArgs A, int accInSmem) {\n"
         "  cltk::b200::path_body<"
      << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false") << ", cltk::b200::JitPayoff, "
-     << pb << ", " << (pb > 1 ? slots : 0) << ", " << (prog.faultBuild ? "true" : "false")
-     << ", " << (h.reg_acc ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
+     << (prog.faultBuild ? "true" : "false")
+     << ", " << (h.reg_acc ? 1 : 0) << ", " << (h.stream ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
   // Shared-memory register columns: only the registers the generated code
   // stores or loads (JW / JR) or the outputs read; the rest live in locals.
   std::string src = os.str();

@@ -124,6 +124,8 @@ typedef struct {
                             // (n_thread; the NVRTC kernel: only the registers it stores)
   uint32_t reg_acc;         // path kernel: 1 = one output, short paths: per-thread register
                             // accumulation of the output, one warp sum per chunk
+  uint32_t stream;          // path kernel: 1 = short Philox paths: a thread's paths of a
+                            // chunk drawn as one stream of full normal batches
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
