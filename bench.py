@@ -33,11 +33,15 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 # FP64 flops per path of the fused kernel, frozen from the ncu SASS op counters
 # (dadd + dmul + 2*dfma) of the first correct kernel (profiles/).
-F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": None,
-          "worst_off_batch": None}
+F_PATH = {"brc": 286221.4, "worst_off": 3069.1, "call": 202.1, "brc_batch": 243.9,
+          "worst_off_batch": 9.6}
 # brc: ncu r1 (profiles/r1_path_kernel_brc_2M_raw.csv), 2e6 paths:
 #   dadd 6.2471e10 + dmul 7.0817e10 + 2 * dfma 2.19577e11 thread-instructions
 # worst_off / call: first measurement (profiles/r1_fp64ops_*_2M.csv), 2e6 paths
+# C4 batches: FP64 flops per INSTANCE-path (1024 instances share each path),
+# first measurement (profiles/r2a_fp64ops_*_batch_200k.csv, 2e5 paths x 1024):
+#   brc_batch: dadd 8.8802e9 + dmul 1.15312e10 + 2 * dfma 1.47653e10 -> 243.9
+#   worst_off_batch: dadd 8.2388e8 + dmul 5.9430e8 + 2 * dfma 2.7376e8 -> 9.6
 # QMC mode (Sobol + AS241 + bridge) has its own F_path, frozen from the first
 # measurement (profiles/r1_fp64ops_qmc_brc_2M.csv, 2e6 paths):
 #   dadd 1.61651e10 + dmul 1.73608e10 + 2 * dfma 8.59067e10 thread-instructions
@@ -48,8 +52,17 @@ F_PATH_QMC = {"brc": 102669.7}
 # its ~90 KB program and the partials stay in L2), and the FP64 pipe activity
 # ncu measured there -- the kernel's own pipe utilisation beside the frozen-F
 # roofline fraction.
-NCU_EVIDENCE = {"brc": {"traffic": 222720.0, "fp64_pipe_active": 0.470,
-                        "capture": "profiles/r1j_path_kernel_brc_10M_raw.csv (10M-path launch)"}}
+# executed_f_path: FP64 flops per path the current kernel executes (ncu source
+# page, predicated-on DADD + DMUL + 2 DFMA thread instructions,
+# tools/ncu_fp64_flops.py) -- the second roofline figure beside the frozen one.
+NCU_EVIDENCE = {
+    "brc": {"traffic": 221952.0, "fp64_pipe_active": 0.469, "executed_f_path": 173624.1,
+            "capture": "profiles/r2a_path_kernel_brc_10M_{raw.csv,summary.txt} (10M-path launch)"},
+    "worst_off": {"traffic": 73984.0, "fp64_pipe_active": 0.445, "executed_f_path": 2882.4,
+                  "capture": "profiles/r2b_path_kernel_worst_off_4M_{raw.csv,summary.txt}"},
+    "call": {"traffic": 54016.0, "fp64_pipe_active": 0.403, "executed_f_path": 180.9,
+             "capture": "profiles/r2b_path_kernel_call_40M_{raw.csv,summary.txt}"},
+}
 
 BATCH_N = 1024
 
@@ -366,8 +379,13 @@ def main():
                 "peak_source": "measured DFMA microbenchmark (cltk_fp64_peak), this GPU, burst",
                 "f_path": fpath}
         if ev:
+            ach_x = per_gpu_paths * ev["executed_f_path"] / (t_kern * 1e-3) / 1e12
             roof.update({"traffic_unit": "bytes per launch", "ncu_capture": ev["capture"],
-                         "fp64_pipe_active_ncu": ev["fp64_pipe_active"]})
+                         "fp64_pipe_active_ncu": ev["fp64_pipe_active"],
+                         "achieved_basis": "frozen algorithmic F_path (first correct kernel) x "
+                                           "paths/s; executed: the flops this kernel runs",
+                         "executed_f_path": ev["executed_f_path"],
+                         "achieved_executed": ach_x, "frac_executed": ach_x / peak_tflops})
     else:
         roof = {"bound": "fp64", "achieved": None, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": None, "traffic": None,

@@ -11,8 +11,10 @@ timeout 900 python bench.py > $O/bench_brc.json 2> $O/bench_brc.err
 timeout 600 python bench.py --workload worst_off --paths-per-gpu 16000000 --ref-paths 200000 > $O/bench_worst_off.json 2> $O/bench_worst_off.err
 timeout 600 python bench.py --workload call --paths-per-gpu 100000000 --ref-paths 4000000 > $O/bench_call.json 2> $O/bench_call.err
 timeout 900 python bench.py --workload brc_batch --paths-per-gpu 10000000 --e2e-steps 1 > $O/bench_brc_batch.json 2> $O/bench_brc_batch.err
+timeout 900 python bench.py --workload worst_off_batch --paths-per-gpu 2000000 --e2e-steps 1 > $O/bench_worst_off_batch.json 2> $O/bench_worst_off_batch.err
 timeout 600 python bench.py --rng sobol --paths-per-gpu 50000000 --no-cpu-baseline > $O/bench_brc_qmc.json 2> $O/bench_brc_qmc.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
+timeout 300 python bench.py --gpus 2 --steps 1 --warmup 1 > $O/bench_gpus2.json 2> $O/bench_gpus2.err; echo "rc=$?" >> $O/bench_gpus2.err
 M=smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,gpu__time_duration.sum
 for w in worst_off call; do
   CMD="python bench.py --workload $w --steps 1 --warmup 1 --paths-per-gpu 2000000 --e2e-steps 0 --no-cpu-baseline"
