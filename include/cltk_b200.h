@@ -12,6 +12,13 @@
  * 5 eval); err (may be NULL) receives the reference's message.  Device
  * failures return 4 with a "device: ..." message.
  *
+ * Limit that differs from the reference: models of at most 8 assets
+ * (CLTK_MAX_ASSETS; the reference has no cap, proj/src/pricing.cpp:217-245) --
+ * larger models return 4 (UnsupportedError).  At most 2^40 paths per call, and
+ * 2^32 in the QMC mode.  The pricing functions never change their inputs;
+ * one plan (cltk_plan_*) serves one caller at a time, any number of plans
+ * may run concurrently.
+ *
  * Entry point                replaces (reference interface)
  * -------------------------  -------------------------------------------------
  * cltk_gpu_price             cltk::priceAcrossTime  proj/include/cltk/pricing.hpp:92-98
@@ -24,7 +31,11 @@
  *                            become deterministic chunks any GPU can price.
  * cltk_black_scholes_call    cltk::blackScholesCall proj/include/cltk/pricing.hpp:62-63
  * cltk_debug_*               test hooks: per-path outputs, RNG streams
- *                            (CounterRng proj/include/cltk/pricing.hpp:43-56)
+ *                            (CounterRng proj/include/cltk/pricing.hpp:43-56), the QMC
+ *                            generator's Sobol integers
+ * cltk_plan_set_fault        test hook: the reference's invNormalCdf domain error
+ *                            (proj/src/pricing.cpp:111-113) at a chosen draw
+ * cltk_nccl_version          the NCCL the in-process multi-GPU path loads
  */
 #ifndef CLTK_B200_H
 #define CLTK_B200_H
