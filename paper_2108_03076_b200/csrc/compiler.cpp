@@ -2,6 +2,7 @@
 // compiled with -ffp-contract=off so host-folded constants are the IEEE
 // results the reference computes at run time.
 #include "compiler.hpp"
+#include "engine_types.h"
 
 #include <algorithm>
 #include <cmath>
@@ -1211,6 +1212,18 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
     // per-step bookkeeping costs)
     const uint64_t slots = static_cast<uint64_t>(nSteps) * std::max<uint32_t>(1, nA);
     h.stream = (plan.rng == CLTK_RNG_PHILOX && slots <= kStreamMaxSlots) ? 1u : 0u;
+    if (h.stream) {
+      // draw mask of a batch starting at step s: its SB steps, wrapping into
+      // the next path (a chunk's paths per thread are whole stream periods,
+      // so no batch runs past the chunk)
+      const uint32_t na = std::max<uint32_t>(1, nA);
+      const int SB = batchSteps(static_cast<int>(na));
+      P.streamMask.assign(nSteps, 0u);
+      for (uint32_t s0 = 0; s0 < nSteps; ++s0)
+        for (int t = 0; t < SB; ++t)
+          if (P.steps[(s0 + t) % nSteps].draws == STEP_DRAW)
+            P.streamMask[s0] |= ((1u << na) - 1u) << (t * na);
+    }
   }
   P.kernelNodes = k.nodes.size();
   P.dagNodes = static_cast<uint64_t>(N);

@@ -61,6 +61,7 @@ struct CompiledProgram {
   std::vector<double> sharedConst;     // bit patterns for B/I/E constants
   std::vector<double> instConst;       // [n_instances][n_inst_const]
   std::vector<cltk_output> outputs;    // [n_days]
+  std::vector<uint32_t> streamMask;    // [n_steps] when header.stream (DevPlan::streamMask)
   std::vector<ErrorSite> sites;        // site id -> error (id 0 unused, 1 = domain)
   cltk_plan_header header{};
   uint64_t kernelNodes = 0, dagNodes = 0;

@@ -238,6 +238,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   I.dev.instConst = upload(I.prog.instConst, I.owned);
   I.dev.outputs = upload(I.prog.outputs, I.owned);
   I.dev.bridge = upload(I.prog.bridge, I.owned);
+  I.dev.streamMask = upload(I.prog.streamMask, I.owned);
   if (I.prog.header.rng == CLTK_RNG_SOBOL) {
     std::vector<uint32_t> V(kSobolV, kSobolV + kSobolDims * 32), T5(kSobolDims * 32);
     for (uint32_t d = 0; d < kSobolDims; ++d)

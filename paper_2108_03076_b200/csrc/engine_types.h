@@ -66,6 +66,9 @@ struct DevPlan {
   const cltk_bridge_op* bridge;
   const uint32_t* sobolV;   // [2048][32] direction numbers
   const uint32_t* sobolT5;  // [2048][32] XOR of v[d][0..4] over the set bits of g
+  // Philox normal streams (header.stream): the draw mask of a batch that
+  // starts at step s (its SB steps wrapping into the next path), [n_steps]
+  const uint32_t* streamMask;
 };
 
 struct RunArgs {
