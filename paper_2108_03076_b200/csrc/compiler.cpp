@@ -1212,6 +1212,8 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
     // per-step bookkeeping costs)
     const uint64_t slots = static_cast<uint64_t>(nSteps) * std::max<uint32_t>(1, nA);
     h.stream = (plan.rng == CLTK_RNG_PHILOX && slots <= kStreamMaxSlots) ? 1u : 0u;
+    // template batches: the warp reduces instance-major (engine_device.cuh)
+    h.inst_major = (nInst >= kInstMajorMin && days.size() == 1 && !hasErr) ? 1u : 0u;
     if (h.stream) {
       // draw mask of a batch starting at step s: its SB steps, wrapping into
       // the next path (a chunk's paths per thread are whole stream periods,

@@ -76,6 +76,9 @@ constexpr uint64_t kRegAccMaxDraws = 64;
 // Philox paths of at most this many normal slots (steps x assets) stream
 // through full normal batches (cltk_plan_header::stream).
 constexpr uint64_t kStreamMaxSlots = 64;
+// Template batches of at least this many instances (one valuation day, no
+// error channel) reduce their outputs instance-major (cltk_plan_header::inst_major).
+constexpr uint64_t kInstMajorMin = 32;
 
 struct CompileOptions {
   bool rewrite = true;

@@ -264,8 +264,12 @@ struct Gen {
   // before the write).  Same ops, same order, same IEEE operations (log-domain
   // minima / maxima: bitwise the same results).  Returns the domain (1: log)
   // of every register written in the block.
+  // final: instance-major variant of the instance section -- instance
+  // literals always from the table (per-lane instances), nothing stored; the
+  // registers' final values are handed back instead.
   std::map<uint32_t, int> emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep,
-                               uint32_t block, const char* ind) const {
+                               uint32_t block, const char* ind,
+                               std::map<uint32_t, std::string>* final = nullptr) const {
     std::map<uint32_t, Val> cur;
     std::map<uint32_t, Val> slotVal;  // materialised spots of this block
     std::set<uint32_t> dirty, carried;
@@ -297,7 +301,7 @@ struct Gen {
           auto e = ent->second.find(i);
           isLog = e != ent->second.end() && e->second;
         }
-      } else if (!copyInst && i >= nThread + nc && i < nThread + nc + ni) {
+      } else if ((!copyInst || final) && i >= nThread + nc && i < nThread + nc + ni) {
         // instance literals straight from the table (L1-resident, broadcast)
         src = "JI(" + std::to_string(i - nThread - nc) + ")";
       } else {
@@ -344,6 +348,10 @@ struct Gen {
       dirty.insert(o.d);
     }
     std::map<uint32_t, int> exitDom;
+    if (final) {
+      for (uint32_t r : dirty) (*final)[r] = cur[r].val.empty() ? cur[r].log : cur[r].val;
+      return exitDom;
+    }
     for (uint32_t r : dirty) {
       const Val& x = cur[r];
       const bool isLog = x.val.empty();
@@ -508,6 +516,7 @@ std::string jitSource(CompiledProgram& prog) {
      << (g.copyInst ? "true" : "false") << ";\n"
         "  static constexpr bool kLogSpots = "
      << (g.logMode ? "true" : "false") << ";\n"
+        "  static constexpr bool kInstT = true;  // inst_t below (instance-major batches)\n"
         "  template <int NA>\n"
         "  static __device__ __forceinline__ void step(const Frame f, const DevPlan& P,\n"
         "                                              const cltk_step* st, const double (&"
@@ -522,6 +531,26 @@ std::string jitSource(CompiledProgram& prog) {
         "  static __device__ __forceinline__ void inst(const Frame f, const DevPlan& P,\n"
         "                                              uint32_t inst) {\n";
   g.emit(os, instOps, false, instBlock, "    ");
+  os << "  }\n";
+  // Instance-major reduction of template batches (header.inst_major): the
+  // instance section for one (path, instance) returning the day's output; f
+  // is the PATH's frame (its thread's register columns), inst this lane's
+  // instance (engine_device.cuh path_body).
+  os << "  static __device__ __forceinline__ double inst_t(const Frame f, const DevPlan& P,\n"
+        "                                                uint32_t inst) {\n";
+  if (h.inst_major && !prog.outputs.empty()) {
+    std::map<uint32_t, std::string> fin;
+    g.emit(os, instOps, false, instBlock, "    ", &fin);
+    const uint32_t v = prog.outputs[0].val;
+    std::string ret;
+    if (fin.count(v)) ret = fin[v];
+    else if (v < h.n_thread) ret = "JR(" + std::to_string(v) + ")";
+    else if (v >= instLo && v < instHi) ret = "JI(" + std::to_string(v - instLo) + ")";
+    else ret = "JC(" + std::to_string(v) + ")";
+    os << "    return " << ret << ";\n";
+  } else {
+    os << "    return 0.0;\n";
+  }
   os << "  }\n};\n}  // namespace\n}  // namespace b200\n}  // namespace cltk\n"
         "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, "
      << (h.rng == CLTK_RNG_SOBOL ? "CLTK_QMC_MIN_BLOCKS" : "CLTK_MIN_BLOCKS") << ")\n"
@@ -529,7 +558,8 @@ std::string jitSource(CompiledProgram& prog) {
         "  cltk::b200::path_body<"
      << nA << ", " << (h.rng == CLTK_RNG_SOBOL ? "true" : "false") << ", cltk::b200::JitPayoff, "
      << (prog.faultBuild ? "true" : "false")
-     << ", " << (h.reg_acc ? 1 : 0) << ", " << (h.stream ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
+     << ", " << (h.reg_acc ? 1 : 0) << ", " << (h.stream ? 1 : 0) << ", "
+     << (h.inst_major ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
   // Shared-memory register columns: only the registers the generated code
   // stores or loads (JW / JR) or the outputs read; the rest live in locals.
   std::string src = os.str();

@@ -126,6 +126,8 @@ typedef struct {
                             // accumulation of the output, one warp sum per chunk
   uint32_t stream;          // path kernel: 1 = short Philox paths: a thread's paths of a
                             // chunk drawn as one stream of full normal batches
+  uint32_t inst_major;      // path kernel: 1 = template batch (many instances, one day, no
+                            // error channel): instance-major output reduction
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
