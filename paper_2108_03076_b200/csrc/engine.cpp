@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 
@@ -57,16 +58,20 @@ void devFree(void* p) {
   if (p) cudaFreeAsync(p, 0);
 }
 
-template <class T>
-T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
-  if (v.empty()) return nullptr;
-  void* p = devMalloc(v.size() * sizeof(T));
-  ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
-  owned.push_back(p);
-  return static_cast<T*>(p);
-}
 
 constexpr uint64_t kMaxChunks = 1ULL << 20;
+
+// Host staging of a plan's arrays, each 256-byte aligned in one block.
+struct Staging {
+  std::vector<char> bytes;
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    const size_t o = (bytes.size() + 255) / 256 * 256;
+    bytes.resize(o + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(bytes.data() + o, v.data(), v.size() * sizeof(T));
+    return o;
+  }
+};
 
 // Philox2x64-10 on the host (QMC digital shifts only).
 uint64_t philoxHost(uint64_t key, uint64_t c0, uint64_t c1) {
@@ -85,6 +90,38 @@ constexpr size_t kJitAutoMaxOps = 4096;          // JIT_AUTO: larger programs st
 
 extern const uint32_t kSobolDims;  // sobol_table.cpp (generated)
 extern const uint32_t kSobolV[];
+
+namespace {
+// The QMC direction numbers (and the 5-bit XOR table of the warp-cooperative
+// skip-ahead), uploaded once per device and kept for the process.
+struct SobolTables {
+  const uint32_t* V = nullptr;
+  const uint32_t* T5 = nullptr;
+};
+const SobolTables& sobolTables(int dev) {
+  static std::mutex mu;
+  static auto& tabs = *new std::map<int, SobolTables>();
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = tabs.find(dev);
+  if (it != tabs.end()) return it->second;
+  std::vector<uint32_t> V(kSobolV, kSobolV + kSobolDims * 32), T5(kSobolDims * 32);
+  for (uint32_t d = 0; d < kSobolDims; ++d)
+    for (uint32_t g = 0; g < 32; ++g) {
+      uint32_t x = 0;
+      for (uint32_t k = 0; k < 5; ++k)
+        if ((g >> k) & 1u) x ^= V[d * 32 + k];
+      T5[d * 32 + g] = x;
+    }
+  void* p = nullptr;
+  ck(cudaMalloc(&p, (V.size() + T5.size()) * sizeof(uint32_t)), "cudaMalloc");
+  ck(cudaMemcpy(p, V.data(), V.size() * sizeof(uint32_t), cudaMemcpyHostToDevice), "H2D");
+  ck(cudaMemcpy(static_cast<uint32_t*>(p) + V.size(), T5.data(), T5.size() * sizeof(uint32_t),
+                cudaMemcpyHostToDevice),
+     "H2D");
+  SobolTables t{static_cast<const uint32_t*>(p), static_cast<const uint32_t*>(p) + V.size()};
+  return tabs.emplace(dev, t).first->second;
+}
+}  // namespace
 
 struct PlanImpl {
   CompiledProgram prog;
@@ -232,31 +269,37 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   PlanImpl::DeviceGuard g(dev);
   ck(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, dev), "attr");
   I.dev.hdr = I.prog.header;
-  I.dev.steps = upload(I.prog.steps, I.owned);
-  I.dev.code = upload(I.prog.packed, I.owned);
-  I.dev.sharedConst = upload(I.prog.sharedConst, I.owned);
-  I.dev.instConst = upload(I.prog.instConst, I.owned);
-  I.dev.outputs = upload(I.prog.outputs, I.owned);
-  I.dev.bridge = upload(I.prog.bridge, I.owned);
-  I.dev.streamMask = upload(I.prog.streamMask, I.owned);
+  // The program in one device block with one upload (a one-shot call pays
+  // one allocation and one copy, not one per array); the error word starts
+  // as "none" (all ones), the chunk counter at 0.
+  {
+    Staging st;
+    const size_t oSteps = st.add(I.prog.steps), oCode = st.add(I.prog.packed),
+                 oShared = st.add(I.prog.sharedConst), oInst = st.add(I.prog.instConst),
+                 oOut = st.add(I.prog.outputs), oBridge = st.add(I.prog.bridge),
+                 oMask = st.add(I.prog.streamMask);
+    const size_t oErr = st.add(std::vector<unsigned long long>{~0ULL, 0ULL});
+    char* base = static_cast<char*>(devMalloc(st.bytes.size()));
+    I.owned.push_back(base);
+    ck(cudaMemcpy(base, st.bytes.data(), st.bytes.size(), cudaMemcpyHostToDevice),
+       "cudaMemcpy H2D");
+    auto at = [&](size_t o, bool nonEmpty) { return nonEmpty ? base + o : nullptr; };
+    I.dev.steps = reinterpret_cast<const cltk_step*>(at(oSteps, !I.prog.steps.empty()));
+    I.dev.code = reinterpret_cast<const uint64_t*>(at(oCode, !I.prog.packed.empty()));
+    I.dev.sharedConst = reinterpret_cast<const double*>(at(oShared, !I.prog.sharedConst.empty()));
+    I.dev.instConst = reinterpret_cast<const double*>(at(oInst, !I.prog.instConst.empty()));
+    I.dev.outputs = reinterpret_cast<const cltk_output*>(at(oOut, !I.prog.outputs.empty()));
+    I.dev.bridge = reinterpret_cast<const cltk_bridge_op*>(at(oBridge, !I.prog.bridge.empty()));
+    I.dev.streamMask = reinterpret_cast<const uint32_t*>(at(oMask, !I.prog.streamMask.empty()));
+    I.errKey = reinterpret_cast<unsigned long long*>(base + oErr);
+    I.chunkCounter = I.errKey + 1;
+  }
   if (I.prog.header.rng == CLTK_RNG_SOBOL) {
-    std::vector<uint32_t> V(kSobolV, kSobolV + kSobolDims * 32), T5(kSobolDims * 32);
-    for (uint32_t d = 0; d < kSobolDims; ++d)
-      for (uint32_t g = 0; g < 32; ++g) {
-        uint32_t x = 0;
-        for (uint32_t k = 0; k < 5; ++k)
-          if ((g >> k) & 1u) x ^= V[d * 32 + k];
-        T5[d * 32 + g] = x;
-      }
-    I.dev.sobolV = upload(V, I.owned);
-    I.dev.sobolT5 = upload(T5, I.owned);
+    const SobolTables& t = sobolTables(dev);
+    I.dev.sobolV = t.V;
+    I.dev.sobolT5 = t.T5;
   }
   void* p = nullptr;
-  p = devMalloc(2 * sizeof(unsigned long long));
-  I.owned.push_back(p);
-  I.errKey = static_cast<unsigned long long*>(p);
-  I.chunkCounter = I.errKey + 1;
-  ck(cudaMemset(I.errKey, 0xff, sizeof(unsigned long long)), "cudaMemset");
   // [n_out] results, then the [kCombineSplit][n_out] combine intermediates
   p = devMalloc((1 + kCombineSplit) * std::max<size_t>(1, I.nOut) * sizeof(cltk_partial));
   I.owned.push_back(p);
