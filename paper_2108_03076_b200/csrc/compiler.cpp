@@ -326,6 +326,8 @@ class Builder {
     auto key = std::make_pair(static_cast<int>(c), m);
     auto it = siteIdx.find(key);
     if (it != siteIdx.end()) return it->second;
+    // the device error word is path << 24 | site (engine_device.cuh)
+    if (sites.size() >= (1u << 24)) throw UnsupportedError("more than 2^24 error sites");
     sites.push_back({c, m});
     uint32_t id = static_cast<uint32_t>(sites.size() - 1);
     siteIdx.emplace(key, id);
@@ -1214,6 +1216,12 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
     h.stream = (plan.rng == CLTK_RNG_PHILOX && slots <= kStreamMaxSlots) ? 1u : 0u;
     // template batches: the warp reduces instance-major (engine_device.cuh)
     h.inst_major = (nInst >= kInstMajorMin && days.size() == 1 && !hasErr) ? 1u : 0u;
+    h.first_draw = nSteps;
+    for (uint32_t s0 = 0; s0 < nSteps; ++s0)
+      if (P.steps[s0].draws == STEP_DRAW) {
+        h.first_draw = s0;
+        break;
+      }
     if (h.stream) {
       // draw mask of a batch starting at step s: its SB steps, wrapping into
       // the next path (a chunk's paths per thread are whole stream periods,

@@ -128,6 +128,8 @@ typedef struct {
                             // chunk drawn as one stream of full normal batches
   uint32_t inst_major;      // path kernel: 1 = template batch (many instances, one day, no
                             // error channel): instance-major output reduction
+  uint32_t first_draw;      // first step that draws (per-path normal batches start there:
+                            // the leading non-drawing steps -- day 0 -- take no slots)
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
