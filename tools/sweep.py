@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-RATE = {"call": 1.2e10, "worst_off": 2.6e9, "brc": 5.4e7}  # paths/s, to bound the sweep
+RATE = {"call": 5.0e10, "worst_off": 3.6e9, "brc": 6.2e7}  # paths/s, to bound the sweep
 out = os.path.join(ROOT, "gpurun_out", "sweep.jsonl")
 os.makedirs(os.path.dirname(out), exist_ok=True)
 for w in ("call", "worst_off", "brc"):
