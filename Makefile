@@ -10,9 +10,12 @@ OBJ      := build/obj
 LIB      := $(PKG)/libcltk_b200.so
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 
-CXXFLAGS := -std=c++17 -O2 -fPIC -ffp-contract=off -Wall -Wno-unused-function \
+# EXTRA_DEFS: experiment builds (e.g. make lib OBJ=build/obj_x LIB=build/variants/x/libcltk_b200.so
+# EXTRA_DEFS=-DCLTK_BLOCK=64); the product build leaves it empty
+EXTRA_DEFS ?=
+CXXFLAGS := $(EXTRA_DEFS) -std=c++17 -O2 -fPIC -ffp-contract=off -Wall -Wno-unused-function \
             -I$(NLOHMANN) -I/usr/local/cuda/include -Iinclude
-NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -ccbin $(HOSTCXX) \
+NVFLAGS  := $(EXTRA_DEFS) $(ARCH) -std=c++17 -O3 -lineinfo -fmad=false -ccbin $(HOSTCXX) \
             -Xcompiler -fPIC -Xptxas -v -Iinclude
 
 HOST_SRCS := host_model compiler engine capi sobol_table jit reindex nccl_comm

@@ -9,7 +9,10 @@
 namespace cltk {
 namespace b200 {
 
-constexpr int kBlock = 128;  // threads per CTA (4 warps)
+#ifndef CLTK_BLOCK
+#define CLTK_BLOCK 128
+#endif
+constexpr int kBlock = CLTK_BLOCK;  // threads per CTA (4 warps)
 constexpr int kWarps = kBlock / 32;
 
 // Normal draws per thread of one warp-cooperative batch (engine_device.cuh).

@@ -86,6 +86,16 @@ const char* kStdintStub =
     "typedef unsigned short uint16_t; typedef short int16_t;\n"
     "typedef unsigned char uint8_t; typedef signed char int8_t;\n";
 
+// The fixed NVRTC options (part of the on-disk cache key): the CTA size the
+// host library was built for is compiled in (shared-memory layout, launch
+// bounds), so libraries built for different sizes never share a cubin.
+const std::vector<std::string>& nvrtcOptions() {
+  static const std::vector<std::string> o = {"-arch=sm_100a", "-std=c++17", "-fmad=false",
+                                             "-lineinfo", "-DCLTK_JIT=1",
+                                             "-DCLTK_BLOCK=" + std::to_string(kBlock)};
+  return o;
+}
+
 std::vector<uint8_t> compileCubin(const std::string& src, std::string* log) {
   Nvrtc& n = nvrtc();
   if (!n.ok) throw UnsupportedError("jit: " + n.why);
@@ -107,8 +117,8 @@ std::vector<uint8_t> compileCubin(const std::string& src, std::string* log) {
     std::istringstream is(f);
     for (std::string t; is >> t;) extra.push_back(t);
   }
-  std::vector<const char*> opts = {"-arch=sm_100a", "-std=c++17", "-fmad=false", "-lineinfo",
-                                   "-DCLTK_JIT=1"};
+  std::vector<const char*> opts;
+  for (const std::string& o : nvrtcOptions()) opts.push_back(o.c_str());
   for (const std::string& t : extra) opts.push_back(t.c_str());
   r = n.compile(prog, static_cast<int>(opts.size()), opts.data());
   size_t ls = 0;
@@ -607,6 +617,7 @@ std::string cachePath(const std::string& src) {
   if (dir.empty()) return "";
   uint64_t h = fnv1a(0xCBF29CE484222325ULL, src);
   for (int i = 0; i < kJitHeaderCount; ++i) h = fnv1a(h, kJitHeaderSources[i]);
+  for (const std::string& o : nvrtcOptions()) h = fnv1a(h, o);
   if (const char* f = std::getenv("CLTK_JIT_FLAGS")) h = fnv1a(h, f);
   char name[40];
   std::snprintf(name, sizeof name, "/%016llx.cubin", static_cast<unsigned long long>(h));
