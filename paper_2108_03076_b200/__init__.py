@@ -548,7 +548,7 @@ def debug_math(fn: str, x, device: int = -1):
     ``fmin(exp(m), exp(x))`` / ``fmax``."""
     import numpy as np
     code = {"exp": 0, "log": 1, "erfc": 2, "inv_normal": 3, "div": 4, "halley_arg": 5,
-            "log_fmin": 6, "log_fmax": 7}[fn]
+            "log_fmin": 6, "log_fmax": 7, "log_fmin_b": 8, "log_fmax_b": 9}[fn]
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.zeros_like(x)
     err = _native.ErrorC()

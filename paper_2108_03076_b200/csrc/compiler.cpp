@@ -1216,6 +1216,23 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
     h.stream = (plan.rng == CLTK_RNG_PHILOX && slots <= kStreamMaxSlots) ? 1u : 0u;
     // template batches: the warp reduces instance-major (engine_device.cuh)
     h.inst_major = (nInst >= kInstMajorMin && days.size() == 1 && !hasErr) ? 1u : 0u;
+    // log-spot range: |logS_j - log(spot_j)| <= sum over drawing steps of
+    // |A_sj| + B_sj * sum_l |L_jl| * zmax, zmax = 8.5 > |invNormalCdf(2^-54)|
+    // (the most extreme normal the generator can draw: uniforms lie in
+    // [2^-54, 1 - 2^-54])
+    h.log_bounded = 0;
+    if (plan.rng == CLTK_RNG_PHILOX) {
+      bool ok = true;
+      for (uint32_t j = 0; j < nA && ok; ++j) {
+        double lsum = 0.0;
+        for (uint32_t l = 0; l <= j; ++l) lsum += std::fabs(plan.chol[j * CLTK_MAX_ASSETS + l]);
+        double cum = std::fabs(plan.logS0[j]);
+        for (const cltk_step& st : P.steps)
+          if (st.draws == STEP_DRAW) cum += std::fabs(st.A[j]) + std::fabs(st.B[j]) * lsum * 8.5;
+        ok = std::isfinite(cum) && cum < 500.0;
+      }
+      h.log_bounded = ok ? 1u : 0u;
+    }
     h.first_draw = nSteps;
     for (uint32_t s0 = 0; s0 < nSteps; ++s0)
       if (P.steps[s0].draws == STEP_DRAW) {

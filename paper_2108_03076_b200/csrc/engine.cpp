@@ -566,7 +566,7 @@ void debugRng(int device, uint64_t seed, uint64_t path, uint64_t i0, uint64_t n,
 }
 
 void debugMath(int device, int fn, const double* x, uint64_t n, double* out) {
-  if (fn < 0 || fn > 7) throw UnsupportedError("debug_math: unknown function " + std::to_string(fn));
+  if (fn < 0 || fn > 9) throw UnsupportedError("debug_math: unknown function " + std::to_string(fn));
   if ((fn == 4 || fn >= 6) && (n % 2) != 0)
     throw UnsupportedError("debug_math: div / log_fmin / log_fmax take pairs");
   if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");

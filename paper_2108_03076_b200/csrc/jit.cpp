@@ -325,7 +325,8 @@ struct Gen {
       Val x = operand(i);
       if (!x.val.empty()) return x.val;
       const std::string v = fresh();
-      os << ind << "const double " << v << " = spot_exp(" << x.log << ");\n";
+      os << ind << "const double " << v << " = " << (prog.header.log_bounded ? "spot_exp_b(" : "spot_exp(")
+         << x.log << ");\n";
       x.val = v;
       if (i < nA && inStep && sRegs) slotVal[i] = x;
       else cur[i] = x;
@@ -340,7 +341,9 @@ struct Gen {
       } else if (lm && (o.op == OP_MIN || o.op == OP_MAX) && !operand(o.a).log.empty() &&
                  !operand(o.b).log.empty()) {
         const std::string a = operand(o.a).log, b = operand(o.b).log;
-        os << ind << "const double " << t << " = " << (o.op == OP_MIN ? "log_fmin(" : "log_fmax(")
+        const char* fn = prog.header.log_bounded ? (o.op == OP_MIN ? "log_fmin_b(" : "log_fmax_b(")
+                                                 : (o.op == OP_MIN ? "log_fmin(" : "log_fmax(");
+        os << ind << "const double " << t << " = " << fn
            << a << ", " << b << ");\n";
         res = Val{t, ""};
       } else {

@@ -130,6 +130,9 @@ typedef struct {
                             // error channel): instance-major output reduction
   uint32_t first_draw;      // first step that draws (per-path normal batches start there:
                             // the leading non-drawing steps -- day 0 -- take no slots)
+  uint32_t log_bounded;     // 1: every path's log-spots provably stay in (-500, 500)
+                            // (host bound over the largest normal): the NVRTC payoff's
+                            // log-domain ops need no range checks
   double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
