@@ -22,7 +22,9 @@
 #define CLTK_OP_BITS 8
 #define CLTK_FIELD_BITS 14
 #define CLTK_MAX_OPERANDS (1 << CLTK_FIELD_BITS)
+#ifndef CLTK_MAX_ASSETS
 #define CLTK_MAX_ASSETS 8
+#endif
 
 // Value kinds in the 8-byte register slots: R = IEEE double; B = double 0/1;
 // I = int64 bit pattern (KExpr int values, proj/src/kernel.cpp:187);
