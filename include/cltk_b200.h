@@ -12,10 +12,11 @@
  * 5 eval); err (may be NULL) receives the reference's message.  Device
  * failures return 4 with a "device: ..." message.
  *
- * Limit that differs from the reference: models of at most 8 assets
- * (CLTK_MAX_ASSETS; the reference has no cap, proj/src/pricing.cpp:217-245) --
- * larger models return 4 (UnsupportedError).  At most 2^40 paths per call, and
- * 2^32 in the QMC mode.  The pricing functions never change their inputs;
+ * Limits that differ from the reference: models of at most 16 assets
+ * (CLTK_MAX_ASSETS; the reference has no cap, proj/src/pricing.cpp:217-245);
+ * models of 9..16 assets run the NVRTC payoff kernel only (jit = 0 and the
+ * QMC mode take at most 8) -- beyond that the call returns 4
+ * (UnsupportedError).  At most 2^40 paths per call, and 2^32 in the QMC mode.  The pricing functions never change their inputs;
  * one plan (cltk_plan_*) serves one caller at a time, any number of plans
  * may run concurrently.
  *

@@ -159,6 +159,9 @@ SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& model, uint32_t rng) 
   if (n > CLTK_MAX_ASSETS)
     throw UnsupportedError("engine supports at most " + std::to_string(CLTK_MAX_ASSETS) +
                            " model assets, model has " + std::to_string(n));
+  if (rng == CLTK_RNG_SOBOL && n > CLTK_AOT_MAX_ASSETS)
+    throw UnsupportedError("QMC mode supports at most " + std::to_string(CLTK_AOT_MAX_ASSETS) +
+                           " model assets, model has " + std::to_string(n));
   p.nAssets = static_cast<uint32_t>(n);
   for (std::size_t i = 0; i < n; ++i)
     for (std::size_t j = 0; j < n; ++j) p.chol[i * CLTK_MAX_ASSETS + j] = chol[i][j];

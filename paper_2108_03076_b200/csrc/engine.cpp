@@ -227,18 +227,23 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   // JIT_AUTO keeps the interpreter's copy in case NVRTC or the module load fails
   std::vector<cltk_step> interpSteps;
   cltk_plan_header interpHdr{};
+  // models of more than CLTK_AOT_MAX_ASSETS assets have no ahead-of-time kernel
+  const bool bigModel = I.prog.header.n_assets > CLTK_AOT_MAX_ASSETS;
+  if (bigModel && opt.jit == JIT_OFF)
+    throw UnsupportedError("models of more than " + std::to_string(CLTK_AOT_MAX_ASSETS) +
+                           " assets need the NVRTC payoff kernel (jit)");
   if (opt.jit != JIT_OFF) {
     std::string why;
     bool use = jitAvailable(&why);
-    if (use && opt.jit == JIT_AUTO && jitOpCount(I.prog) > kJitAutoMaxOps) use = false;
-    if (!use && opt.jit == JIT_ON) throw UnsupportedError("jit: " + why);
+    if (use && opt.jit == JIT_AUTO && !bigModel && jitOpCount(I.prog) > kJitAutoMaxOps) use = false;
+    if (!use && (opt.jit == JIT_ON || bigModel)) throw UnsupportedError("jit: " + why);
     if (use) {
       interpSteps = I.prog.steps;
       interpHdr = I.prog.header;
       try {
         jitSrc = jitSource(I.prog);  // assigns steps[].jit_class (uploaded below)
       } catch (const Error&) {
-        if (opt.jit == JIT_ON) throw;
+        if (opt.jit == JIT_ON || bigModel) throw;
         jitSrc.clear();
         I.prog.steps = interpSteps;
         I.prog.header = interpHdr;
@@ -254,7 +259,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
     try {
       I.jitFn = jitKernel(jitSrc);
     } catch (const Error&) {
-      if (opt.jit == JIT_ON) throw;
+      if (opt.jit == JIT_ON || bigModel) throw;
       cudaGetLastError();
       jitSrc.clear();
       I.jitFn = nullptr;
@@ -520,6 +525,9 @@ void planSetErrorWord(Plan& plan, void* stream, uint64_t word) {
 uint64_t debugPaths(Plan& plan, uint64_t seed, uint64_t path0, uint64_t npaths, double* outputs,
                     double* spots, double* normals) {
   PlanImpl& I = *plan.impl();
+  if (I.prog.header.n_assets > CLTK_AOT_MAX_ASSETS)
+    throw UnsupportedError("debug_paths: at most " + std::to_string(CLTK_AOT_MAX_ASSETS) +
+                           " model assets (ahead-of-time kernel)");
   PlanImpl::DeviceGuard g(I.device);
   const cltk_plan_header& h = I.prog.header;
   const size_t nS = static_cast<size_t>(npaths) * h.n_steps * std::max<uint32_t>(1, h.n_assets);

@@ -22,9 +22,12 @@
 #define CLTK_OP_BITS 8
 #define CLTK_FIELD_BITS 14
 #define CLTK_MAX_OPERANDS (1 << CLTK_FIELD_BITS)
+// Models of up to 16 assets; the ahead-of-time (interpreter) kernels and the
+// QMC mode cover up to CLTK_AOT_MAX_ASSETS, larger models run the NVRTC kernel.
 #ifndef CLTK_MAX_ASSETS
-#define CLTK_MAX_ASSETS 8
+#define CLTK_MAX_ASSETS 16
 #endif
+#define CLTK_AOT_MAX_ASSETS 8
 
 // Value kinds in the 8-byte register slots: R = IEEE double; B = double 0/1;
 // I = int64 bit pattern (KExpr int values, proj/src/kernel.cpp:187);

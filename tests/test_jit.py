@@ -50,7 +50,8 @@ def test_brc_source_structure():
     cases = re.findall(r"case (\d+): \{", src)
     assert len(cases) == 3, cases
     # spots arrive as logarithms; the running minima stay in the log domain
-    assert "kLogSpots = true" in src and "L[0]" in src and "log_fmin(" in src
+    # (log_fmin_b: the range-checked form is dropped when the host bounds the log-spots)
+    assert "kLogSpots = true" in src and "L[0]" in src and ("log_fmin(" in src or "log_fmin_b(" in src)
     for lit in ("2630.635", "8288", "840"):
         assert lit not in src
     # a different literal instance of the template: identical source
@@ -159,7 +160,7 @@ def _up_barrier_brc():
 
 def test_up_barrier_source_uses_log_fmax():
     src = E.jit_source(E.Kernel(_up_barrier_brc()), load_model("three"), [0, 100])
-    assert "log_fmax(" in src and "kLogSpots = true" in src
+    assert ("log_fmax(" in src or "log_fmax_b(" in src) and "kLogSpots = true" in src
 
 
 @pytest.mark.gpu
