@@ -27,5 +27,8 @@ if [ "${1:-}" = "full" ]; then
   # one full capture of the hot kernel (smaller step so the ~40 replays stay short)
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:path -s 3 -c 1 \
     -o $O/brc_full python bench.py --steps 1 --warmup 3 --paths-per-gpu 10000000 --e2e-steps 0 --no-cpu-baseline > $O/ncu_full.log 2>&1
+  bash tools/ncu_wl.sh wo_full worst_off 4000000
+  bash tools/ncu_wl.sh call_full call 40000000
+  bash tools/ncu_qmc.sh qmc_full
 fi
 echo done
