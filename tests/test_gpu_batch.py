@@ -53,3 +53,35 @@ def test_instance_major_batch_is_shard_invariant():
     lits = _table(k, 40)
     one = E.price_template(k, lits, m, 123_457, 3, [0])
     assert E.price_template(k, lits, m, 123_457, 3, [0], devices=[0, 0, 0]) == one
+
+
+@pytest.mark.parametrize("kern,paths", [("worst-off", 20_000), ("brc", 2_000)])
+def test_instance_major_batch_qmc_modes_bitwise(kern, paths):
+    """The QMC mode's instance-major batches: the interpreter parks 16 rows
+    (X, P and the bridge rows) instead of 12 -- still the same values in the
+    same order as the NVRTC kernel."""
+    k = load_kernel(kern)
+    m = load_model("three")
+    lits = _table(k, 40)
+    jit = E.price_template(k, lits, m, paths, 5, [0], rng="sobol", jit=True)
+    interp = E.price_template(k, lits, m, paths, 5, [0], rng="sobol", jit=False)
+    assert jit == interp
+    one = E.price_template(k, [lits[7]], m, paths, 5, [0], rng="sobol")[0][0]
+    assert abs(jit[7][0]["price"] - one["price"]) <= PRICE_REL * abs(one["price"])
+
+
+def test_stream_mode_multi_day_and_template_modes_bitwise():
+    """Short paths (normal streams) with several valuation days and a small
+    template table (< 32 instances: path-major reduction, parked in the P/Y
+    rows while X still holds the stream's next normals)."""
+    k = load_kernel("worst-off")
+    m = load_model("three")
+    lits = _table(k, 5)
+    days = [0, 73, 200, 365]
+    jit = E.price_template(k, lits, m, 50_001, 9, days, jit=True)
+    interp = E.price_template(k, lits, m, 50_001, 9, days, jit=False)
+    assert jit == interp
+    for i in (0, 4):
+        one = E.price_template(k, [lits[i]], m, 50_001, 9, days)[0]
+        for a, b in zip(jit[i], one):
+            assert a["price"] == b["price"] and a["std_error"] == b["std_error"]
