@@ -364,7 +364,9 @@ def main():
     n_chunks = pricer.plan.chunking(paths)[1]
     n_launches = 1 + (2 if (n_chunks + 4095) // 4096 > 1 else 1)
     L = pricer.plan.dump()
-    h2d = (len(L["ops"]) * 8 + len(L["steps"]) * 224 + (L["n_shared_const"] + L["n_inst_const"]) * 8
+    step_bytes = 32 + 24 * ((max(1, L["n_assets"]) + 1) // 2 * 2)  # device step records
+    h2d = (len(L["ops"]) * 8 + len(L["steps"]) * step_bytes
+           + (L["n_shared_const"] + L["n_inst_const"]) * 8
            + len(L["outputs"]) * 8 + 16 + len(kern_json) * 0)
     d2h = info["n_outputs"] * 24 + 8
 

@@ -61,6 +61,28 @@ void devFree(void* p) {
 
 constexpr uint64_t kMaxChunks = 1ULL << 20;
 
+// The device step records (engine_types.h StepRef): header + A, B, S of the
+// plan's assets, padded to an even count.
+std::vector<unsigned char> packSteps(const std::vector<cltk_step>& steps, uint32_t nAssets) {
+  const int na = nAssets ? static_cast<int>(nAssets) : 1;
+  const size_t stride = stepStride(na), pad = static_cast<size_t>(stepPad(na));
+  std::vector<unsigned char> out(steps.size() * stride, 0);
+  for (size_t s = 0; s < steps.size(); ++s) {
+    const cltk_step& st = steps[s];
+    const cltk_step_hdr h{st.draws,  st.code_begin, st.code_end,  st.br_begin,
+                          st.br_end, st.br_emit,    st.jit_class, st.draw_window};
+    unsigned char* b = out.data() + s * stride;
+    std::memcpy(b, &h, sizeof h);
+    double* a = reinterpret_cast<double*>(b + sizeof h);
+    for (int j = 0; j < na; ++j) {
+      a[j] = st.A[j];
+      a[pad + j] = st.B[j];
+      a[2 * pad + j] = st.S[j];
+    }
+  }
+  return out;
+}
+
 // Host staging of a plan's arrays, each 256-byte aligned in one block.
 struct Staging {
   std::vector<char> bytes;
@@ -279,7 +301,8 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   // as "none" (all ones), the chunk counter at 0.
   {
     Staging st;
-    const size_t oSteps = st.add(I.prog.steps), oCode = st.add(I.prog.packed),
+    const size_t oSteps = st.add(packSteps(I.prog.steps, I.prog.header.n_assets)),
+                 oCode = st.add(I.prog.packed),
                  oShared = st.add(I.prog.sharedConst), oInst = st.add(I.prog.instConst),
                  oOut = st.add(I.prog.outputs), oBridge = st.add(I.prog.bridge),
                  oMask = st.add(I.prog.streamMask);
@@ -289,7 +312,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
     ck(cudaMemcpy(base, st.bytes.data(), st.bytes.size(), cudaMemcpyHostToDevice),
        "cudaMemcpy H2D");
     auto at = [&](size_t o, bool nonEmpty) { return nonEmpty ? base + o : nullptr; };
-    I.dev.steps = reinterpret_cast<const cltk_step*>(at(oSteps, !I.prog.steps.empty()));
+    I.dev.steps = reinterpret_cast<const unsigned char*>(at(oSteps, !I.prog.steps.empty()));
     I.dev.code = reinterpret_cast<const uint64_t*>(at(oCode, !I.prog.packed.empty()));
     I.dev.sharedConst = reinterpret_cast<const double*>(at(oShared, !I.prog.sharedConst.empty()));
     I.dev.instConst = reinterpret_cast<const double*>(at(oInst, !I.prog.instConst.empty()));

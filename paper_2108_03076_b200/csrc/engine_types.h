@@ -60,7 +60,7 @@ inline PhiloxKeys philoxKeys(uint64_t seed) {
 // Everything the path kernel reads, all device pointers.
 struct DevPlan {
   cltk_plan_header hdr;
-  const cltk_step* steps;
+  const unsigned char* steps;  // [n_steps] device step records (StepRef)
   const uint64_t* code;
   const double* sharedConst;
   const double* instConst;
@@ -73,6 +73,25 @@ struct DevPlan {
   // starts at step s (its SB steps wrapping into the next path), [n_steps]
   const uint32_t* streamMask;
 };
+
+// Device step records of a plan with NA assets: header, A, B, S (even counts).
+CLTK_TYPES_HD inline constexpr int stepPad(int na) { return ((na < 1 ? 1 : na) + 1) & ~1; }
+CLTK_TYPES_HD inline constexpr size_t stepStride(int na) {
+  return sizeof(cltk_step_hdr) + 3 * sizeof(double) * static_cast<size_t>(stepPad(na));
+}
+struct StepRef {
+  const cltk_step_hdr* h;
+  const double* A;
+  const double* B;
+  const double* S;
+};
+template <int NA>
+CLTK_TYPES_HD inline StepRef stepAt(const unsigned char* steps, uint32_t s) {
+  const unsigned char* b = steps + static_cast<size_t>(s) * stepStride(NA);
+  const double* a = reinterpret_cast<const double*>(b + sizeof(cltk_step_hdr));
+  return StepRef{reinterpret_cast<const cltk_step_hdr*>(b), a, a + stepPad(NA),
+                 a + 2 * stepPad(NA)};
+}
 
 struct RunArgs {
   PhiloxKeys keys;

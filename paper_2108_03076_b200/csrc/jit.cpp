@@ -518,9 +518,9 @@ std::string jitSource(CompiledProgram& prog) {
         "namespace cltk {\nnamespace b200 {\nnamespace {\n"
         "static_assert(sizeof(DevPlan) == "
      << sizeof(DevPlan) << ", \"DevPlan layout\");\nstatic_assert(sizeof(RunArgs) == "
-     << sizeof(RunArgs) << ", \"RunArgs layout\");\nstatic_assert(sizeof(cltk_step) == "
-     << sizeof(cltk_step)
-     << ", \"cltk_step layout\");\n"
+     << sizeof(RunArgs) << ", \"RunArgs layout\");\nstatic_assert(sizeof(cltk_step_hdr) == "
+     << sizeof(cltk_step_hdr)
+     << ", \"cltk_step_hdr layout\");\n"
         "#define JR(i) lds64(f.R + (i) * (kBlock * 8u))\n"
         "#define JW(i, v) sts64(f.R + (i) * (kBlock * 8u), (v))\n"
         "#define JC(i) lds64(f.C + (i) * 8u)\n"
@@ -533,9 +533,9 @@ std::string jitSource(CompiledProgram& prog) {
         "  static constexpr bool kInstT = true;  // inst_t below (instance-major batches)\n"
         "  template <int NA>\n"
         "  static __device__ __forceinline__ void step(const Frame f, const DevPlan& P,\n"
-        "                                              const cltk_step* st, const double (&"
+        "                                              const StepRef st, const double (&"
      << (g.logMode ? "L" : "S") << ")[NA]) {\n"
-        "    switch (__ldg(&st->jit_class)) {\n";
+        "    switch (__ldg(&st.h->jit_class)) {\n";
   for (size_t c = 1; c < classOps.size(); ++c) {
     os << "      case " << c << ": {\n";
     g.emit(os, classOps[c], true, static_cast<uint32_t>(c), "        ");

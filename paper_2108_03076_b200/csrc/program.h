@@ -97,6 +97,21 @@ typedef struct {
   uint32_t draw_window;
 } cltk_step;
 
+// Device layout of the steps (engine_types.h StepRef): per step this header,
+// then A, B and S of the plan's assets (each padded to an even count so the
+// arrays stay 16-byte aligned): 32 + 24 * even(nA) bytes instead of the host
+// struct's 32 + 24 * CLTK_MAX_ASSETS.
+typedef struct {
+  uint32_t draws;
+  uint32_t code_begin;
+  uint32_t code_end;
+  uint32_t br_begin;
+  uint32_t br_end;
+  uint32_t br_emit;
+  uint32_t jit_class;
+  uint32_t draw_window;
+} cltk_step_hdr;
+
 // Brownian-bridge construction op (QMC mode): for every asset j
 //   W[dst][j] = wl * W[l][j] + wr * W[r][j] + sd * Z[c][j]
 // (l == CLTK_BR_ORIGIN: W(0) = 0); Z[c] uses Sobol dimensions node * nA + j.
