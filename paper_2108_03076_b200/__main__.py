@@ -2,7 +2,7 @@
 
     python -m paper_2108_03076_b200 price KERNEL --model MODEL.json [--paths N]
         [--seed S] [--at D ...] [--threads T] [--tenv TENV.json] [--rng philox|sobol]
-        [--jit 0|1|auto] [--device D]
+        [--jit 0|1|auto] [--device D] [--devices D0,D1,...]
 
 Mirrors the reference CLI's `price` subcommand (proj/tools/cli.cpp:155-162,
 246-259): same options and defaults (paths 100000, seed 1, valuation day 0),
@@ -31,8 +31,9 @@ def _price(args) -> int:
             tenv = json.load(f)
     days = args.at or [0]
     jit = {"0": False, "1": True, "auto": "auto"}[args.jit]
+    devices = [int(d) for d in args.devices.split(",") if d.strip()] if args.devices else None
     res = E.price(kernel, model, args.paths, args.seed, days, tenv, threads=args.threads,
-                  device=args.device, rng=args.rng, jit=jit)
+                  device=args.device, rng=args.rng, jit=jit, devices=devices)
     out = [{"price": r["price"], "stdError": r["std_error"], "paths": r["paths"],
             "seed": r["seed"], "valuationDay": r["valuation_day"]} for r in res]
     print(json.dumps(out, separators=(",", ":")))
@@ -53,6 +54,9 @@ def main(argv=None) -> int:
     p.add_argument("--rng", default="philox", choices=["philox", "sobol"])
     p.add_argument("--jit", default="auto", choices=["0", "1", "auto"])
     p.add_argument("--device", type=int, default=-1)
+    p.add_argument("--devices", default=None,
+                   help="shard over these GPUs of this process (comma-separated; one NCCL "
+                        "all-gather; the same bits as one GPU)")
     args = ap.parse_args(argv)
     try:
         return _price(args)

@@ -47,3 +47,8 @@ def test_cli_prices_like_the_api():
     r2 = _run("price", kern, "--model", model, "--paths", "20000", "--seed", "7", "--at", "0",
               "100", "--jit", "1")
     assert json.loads(r2.stdout) == out
+    # sharded over a device list (one GPU listed twice here): the same bits
+    r3 = _run("price", kern, "--model", model, "--paths", "20000", "--seed", "7", "--at", "0",
+              "100", "--devices", "0,0")
+    assert r3.returncode == 0, r3.stderr
+    assert json.loads(r3.stdout) == out
