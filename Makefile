@@ -23,7 +23,7 @@ HOST_OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS))) $(OBJ)/jit_source
 # device headers embedded for the NVRTC build (csrc/jit.cpp)
 JIT_HDRS  := $(SRC)/engine_device.cuh $(SRC)/engine_types.h $(SRC)/program.h \
              $(SRC)/glibc_math.h $(SRC)/glibc_tables.h
-CU_OBJS   := $(OBJ)/mc_engine.o
+CU_OBJS   := $(OBJ)/mc_engine.o $(OBJ)/mc_engine_qmc.o $(OBJ)/mc_engine_fault.o
 HDRS      := $(wildcard $(SRC)/*.hpp $(SRC)/*.h $(SRC)/*.cuh) include/cltk_b200.h
 
 .PHONY: all lib oracle testlib clean
@@ -42,10 +42,11 @@ $(OBJ)/jit_sources.cpp: $(JIT_HDRS) tools/embed_sources.py
 $(OBJ)/jit_sources.o: $(OBJ)/jit_sources.cpp
 	$(HOSTCXX) $(CXXFLAGS) -c $< -o $@
 
-$(OBJ)/mc_engine.o: $(SRC)/mc_engine.cu $(HDRS) $(SRC)/engine_device.cuh
+# three translation units compiled in parallel (mc_engine.cu CLTK_AOT_PART)
+$(OBJ)/mc_engine%.o: $(SRC)/mc_engine%.cu $(SRC)/mc_engine.cu $(HDRS) $(SRC)/engine_device.cuh
 	@mkdir -p $(OBJ)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/mc_engine.ptxas.txt || (cat $(OBJ)/mc_engine.ptxas.txt; false)
-	@grep -E "Used|spill" $(OBJ)/mc_engine.ptxas.txt | head -40
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/mc_engine$*.ptxas.txt || (cat $(OBJ)/mc_engine$*.ptxas.txt; false)
+	@grep -E "Used|spill" $(OBJ)/mc_engine$*.ptxas.txt | head -40
 
 $(LIB): $(HOST_OBJS) $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -cudart static -o $@ $^ -ldl

@@ -6,8 +6,38 @@
 #include "engine_launch.hpp"
 #include "engine_device.cuh"
 
+// Compiled as three translation units (Makefile, in parallel) so the kernel
+// instantiations build concurrently -- this file, and mc_engine_qmc.cu /
+// mc_engine_fault.cu which include it with another CLTK_AOT_PART: 0 -- the Philox path kernels, the dump,
+// combine and test kernels and every host entry point; 1 -- the QMC kernels;
+// 2 -- the fault-hook test build of the Philox kernels.
+#ifndef CLTK_AOT_PART
+#define CLTK_AOT_PART 0
+#endif
+
+#define CLTK_NA_SWITCH(NA_, CALL)                 \
+  switch (NA_) {                                  \
+    case 1: { constexpr int NA = 1; CALL; }       \
+    case 2: { constexpr int NA = 2; CALL; }       \
+    case 3: { constexpr int NA = 3; CALL; }       \
+    case 4: { constexpr int NA = 4; CALL; }       \
+    case 5: { constexpr int NA = 5; CALL; }       \
+    case 6: { constexpr int NA = 6; CALL; }       \
+    case 7: { constexpr int NA = 7; CALL; }       \
+    case 8: { constexpr int NA = 8; CALL; }       \
+    default: { constexpr int NA = 1; CALL; }      \
+  }
+
 namespace cltk {
 namespace b200 {
+
+// (parts 1 and 2)
+cudaError_t launchPathQmc(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
+                          cudaStream_t s, int accInSmem);
+int occupancyQmc(const cltk_plan_header& h, size_t smem);
+cudaError_t launchDumpQmc(const DevPlan& p, const DumpArgs& a, cudaStream_t s);
+cudaError_t launchPathFault(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
+                            cudaStream_t s, int accInSmem);
 
 namespace {
 
@@ -63,6 +93,7 @@ int occupancyT(size_t smem) {
 
 }  // namespace
 
+#if CLTK_AOT_PART == 0
 bool accFitsSmem(const cltk_plan_header& h) {
   const size_t nOut = static_cast<size_t>(h.n_instances) * h.n_days;
   return kWarps * nOut * 3 * sizeof(double) <= 48 * 1024;
@@ -79,22 +110,8 @@ size_t pathKernelSmem(const cltk_plan_header& h, bool accInSmem) {
   return words * sizeof(double);
 }
 
-#define CLTK_NA_SWITCH(NA_, CALL)                 \
-  switch (NA_) {                                  \
-    case 1: { constexpr int NA = 1; CALL; }       \
-    case 2: { constexpr int NA = 2; CALL; }       \
-    case 3: { constexpr int NA = 3; CALL; }       \
-    case 4: { constexpr int NA = 4; CALL; }       \
-    case 5: { constexpr int NA = 5; CALL; }       \
-    case 6: { constexpr int NA = 6; CALL; }       \
-    case 7: { constexpr int NA = 7; CALL; }       \
-    case 8: { constexpr int NA = 8; CALL; }       \
-    default: { constexpr int NA = 1; CALL; }      \
-  }
-
 int pathKernelOccupancy(const cltk_plan_header& h, size_t smem) {
-  if (h.rng == CLTK_RNG_SOBOL)
-    CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return (occupancyT<NA, true>(smem)));
+  if (h.rng == CLTK_RNG_SOBOL) return occupancyQmc(h, smem);
   CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return (occupancyT<NA, false>(smem)));
 }
 
@@ -103,19 +120,15 @@ cudaError_t launchPath(const DevPlan& p, const RunArgs& a, int grid, size_t smem
   const int accInSmem = accFitsSmem(p.hdr) ? 1 : 0;
   if (fault) {  // test builds of the Philox kernels (cltk_plan_set_fault)
     if (p.hdr.rng == CLTK_RNG_SOBOL) return cudaErrorInvalidValue;
-    CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
-                   return (launchPathT<NA, false, true>(p, a, grid, smem, s, accInSmem)));
+    return launchPathFault(p, a, grid, smem, s, accInSmem);
   }
-  if (p.hdr.rng == CLTK_RNG_SOBOL)
-    CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
-                   return (launchPathT<NA, true>(p, a, grid, smem, s, accInSmem)));
+  if (p.hdr.rng == CLTK_RNG_SOBOL) return launchPathQmc(p, a, grid, smem, s, accInSmem);
   CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
                  return (launchPathT<NA, false>(p, a, grid, smem, s, accInSmem)));
 }
 
 cudaError_t launchDump(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
-  if (p.hdr.rng == CLTK_RNG_SOBOL)
-    CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return (launchDumpT<NA, true>(p, a, s)));
+  if (p.hdr.rng == CLTK_RNG_SOBOL) return launchDumpQmc(p, a, s);
   CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return (launchDumpT<NA, false>(p, a, s)));
 }
 
@@ -160,6 +173,30 @@ cudaError_t launchFp64Peak(double* sink, int iters, int grid, cudaStream_t s) {
   fp64_peak_kernel<<<grid, 256, 0, s>>>(sink, iters);
   return cudaGetLastError();
 }
+
+#endif  // CLTK_AOT_PART == 0
+
+#if CLTK_AOT_PART == 1
+cudaError_t launchPathQmc(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
+                          cudaStream_t s, int accInSmem) {
+  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
+                 return (launchPathT<NA, true>(p, a, grid, smem, s, accInSmem)));
+}
+int occupancyQmc(const cltk_plan_header& h, size_t smem) {
+  CLTK_NA_SWITCH(h.n_assets == 0 ? 1 : h.n_assets, return (occupancyT<NA, true>(smem)));
+}
+cudaError_t launchDumpQmc(const DevPlan& p, const DumpArgs& a, cudaStream_t s) {
+  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets, return (launchDumpT<NA, true>(p, a, s)));
+}
+#endif
+
+#if CLTK_AOT_PART == 2
+cudaError_t launchPathFault(const DevPlan& p, const RunArgs& a, int grid, size_t smem,
+                            cudaStream_t s, int accInSmem) {
+  CLTK_NA_SWITCH(p.hdr.n_assets == 0 ? 1 : p.hdr.n_assets,
+                 return (launchPathT<NA, false, true>(p, a, grid, smem, s, accInSmem)));
+}
+#endif
 
 }  // namespace b200
 }  // namespace cltk
