@@ -277,10 +277,15 @@ struct Gen {
   // of every register written in the block.
   // final: instance-major variant of the instance section -- instance
   // literals always from the table (per-lane instances), nothing stored; the
-  // registers' final values are handed back instead.
+  // registers' final values are handed back instead.  The warp constants it
+  // reads are collected in *kc and read as k.c[n]: loaded once per row of
+  // paths (inst_k), not once per (path, instance); the path's registers in
+  // *kr, read as r.c[n] (inst_r: loaded once per path for two instances).
   std::map<uint32_t, int> emit(std::ostringstream& os, const std::vector<DOp>& ops, bool inStep,
                                uint32_t block, const char* ind,
-                               std::map<uint32_t, std::string>* final = nullptr) const {
+                               std::map<uint32_t, std::string>* final = nullptr,
+                               std::vector<uint32_t>* kc = nullptr,
+                               std::vector<uint32_t>* kr = nullptr) const {
     std::map<uint32_t, Val> cur;
     std::map<uint32_t, Val> slotVal;  // materialised spots of this block
     std::set<uint32_t> dirty, carried;
@@ -307,7 +312,12 @@ struct Gen {
       bool isLog = false;
       if (i < nThread) {
         carried.insert(i);
-        src = "JR(" + std::to_string(i) + ")";
+        if (kr) {
+          src = "r.c[" + std::to_string(kr->size()) + "]";
+          kr->push_back(i);
+        } else {
+          src = "JR(" + std::to_string(i) + ")";
+        }
         if (ent != entryDom.end()) {
           auto e = ent->second.find(i);
           isLog = e != ent->second.end() && e->second;
@@ -315,6 +325,9 @@ struct Gen {
       } else if ((!copyInst || final) && i >= nThread + nc && i < nThread + nc + ni) {
         // instance literals straight from the table (L1-resident, broadcast)
         src = "JI(" + std::to_string(i - nThread - nc) + ")";
+      } else if (kc) {
+        src = "k.c[" + std::to_string(kc->size()) + "]";
+        kc->push_back(i);
       } else {
         src = "JC(" + std::to_string(i) + ")";
       }
@@ -550,20 +563,48 @@ std::string jitSource(CompiledProgram& prog) {
   // instance section for one (path, instance) returning the day's output; f
   // is the PATH's frame (its thread's register columns), inst this lane's
   // instance (engine_device.cuh path_body).
-  os << "  static __device__ __forceinline__ double inst_t(const Frame f, const DevPlan& P,\n"
-        "                                                uint32_t inst) {\n";
-  if (h.inst_major && !prog.outputs.empty()) {
-    std::map<uint32_t, std::string> fin;
-    g.emit(os, instOps, false, instBlock, "    ", &fin);
-    const uint32_t v = prog.outputs[0].val;
-    std::string ret;
-    if (fin.count(v)) ret = fin[v];
-    else if (v < h.n_thread) ret = "JR(" + std::to_string(v) + ")";
-    else if (v >= instLo && v < instHi) ret = "JI(" + std::to_string(v - instLo) + ")";
-    else ret = "JC(" + std::to_string(v) + ")";
-    os << "    return " << ret << ";\n";
-  } else {
-    os << "    return 0.0;\n";
+  // The warp constants it reads come in k (inst_k: loaded once per row of
+  // paths by the caller, outside its loops over paths and instances), the
+  // path's register columns in r (inst_r: once per path, shared by the two
+  // instances a lane evaluates).
+  {
+    std::ostringstream body;
+    std::vector<uint32_t> kc, kr;
+    if (h.inst_major && !prog.outputs.empty()) {
+      std::map<uint32_t, std::string> fin;
+      g.emit(body, instOps, false, instBlock, "    ", &fin, &kc, &kr);
+      const uint32_t v = prog.outputs[0].val;
+      std::string ret;
+      if (fin.count(v)) {
+        ret = fin[v];
+      } else if (v < h.n_thread) {
+        ret = "r.c[" + std::to_string(kr.size()) + "]";
+        kr.push_back(v);
+      } else if (v >= instLo && v < instHi) {
+        ret = "JI(" + std::to_string(v - instLo) + ")";
+      } else {
+        ret = "k.c[" + std::to_string(kc.size()) + "]";
+        kc.push_back(v);
+      }
+      body << "    return " << ret << ";\n";
+    } else {
+      body << "    return 0.0;\n";
+    }
+    auto table = [&](const char* type, const char* fn, const char* arg, const char* macro,
+                     const std::vector<uint32_t>& ix) {
+      os << "  struct " << type << " {\n    double c[" << std::max<size_t>(ix.size(), 1)
+         << "];\n  };\n  static __device__ __forceinline__ " << type << " " << fn
+         << "(const Frame f) {\n    " << type << " " << arg << ";\n";
+      for (size_t n = 0; n < ix.size(); ++n)
+        os << "    " << arg << ".c[" << n << "] = " << macro << "(" << ix[n] << ");\n";
+      if (ix.empty()) os << "    " << arg << ".c[0] = 0.0;\n";
+      os << "    return " << arg << ";\n  }\n";
+    };
+    table("InstK", "inst_k", "k", "JC", kc);
+    table("InstR", "inst_r", "r", "JR", kr);
+    os << "  static __device__ __forceinline__ double inst_t(const DevPlan& P, uint32_t inst,\n"
+          "                                                const InstK& k, const InstR& r) {\n"
+       << body.str();
   }
   os << "  }\n};\n}  // namespace\n}  // namespace b200\n}  // namespace cltk\n"
         "extern \"C\" __global__ void __launch_bounds__(cltk::b200::kBlock, "
