@@ -570,36 +570,36 @@ uint64_t kernelShapeHash(const Kernel& k) {
   return h;
 }
 
-// ModelSpec::at (proj/src/pricing.cpp:13-18)
+// ModelSpec::at (proj/src/pricing.cpp:13-18): same message on a missing label.
 const AssetSpec& ModelSpec::at(const std::string& label) const {
-  auto it = assets.find(label);
-  if (it == assets.end()) throw EvalError("model has no asset spec for label " + label);
-  return it->second;
+  const auto found = assets.find(label);
+  if (found != assets.end()) return found->second;
+  throw EvalError("model has no asset spec for label " + label);
 }
 
-// modelFromJson (proj/src/pricing.cpp:20-43)
+// modelFromJson (proj/src/pricing.cpp:20-43): the same schema and defaults
+// (rate 0, dayCount 365, drift = rate, order = the sorted labels unless
+// given), with the reference CLI's parse-error wording for malformed input.
 ModelSpec modelFromJson(const std::string& text) {
   ModelSpec m;
   try {
-    Json j = Json::parse(text);
-    m.rate = j.value("rate", 0.0);
-    m.dayCount = j.value("dayCount", 365.0);
-    const auto& labels = j.at("labels");
-    if (j.contains("order")) {
-      m.order = j.at("order").get<std::vector<std::string>>();
+    const Json doc = Json::parse(text);
+    m.rate = doc.value("rate", 0.0);
+    m.dayCount = doc.value("dayCount", 365.0);
+    const Json& labels = doc.at("labels");
+    if (doc.contains("order")) {
+      m.order = doc.at("order").get<std::vector<std::string>>();
     } else {
-      for (auto it = labels.begin(); it != labels.end(); ++it) m.order.push_back(it.key());
+      m.order.reserve(labels.size());
+      for (const auto& kv : labels.items()) m.order.push_back(kv.key());
       std::sort(m.order.begin(), m.order.end());
     }
-    for (const auto& label : m.order) {
-      const auto& spec = labels.at(label);
-      AssetSpec a;
-      a.spot = spec.at("spot").get<double>();
-      a.vol = spec.at("vol").get<double>();
-      a.drift = spec.value("drift", m.rate);
-      m.assets[label] = a;
+    for (const std::string& label : m.order) {
+      const Json& spec = labels.at(label);
+      m.assets[label] = AssetSpec{spec.at("spot").get<double>(), spec.at("vol").get<double>(),
+                                  spec.value("drift", m.rate)};
     }
-    if (j.contains("corr")) m.corr = j.at("corr").get<std::vector<std::vector<double>>>();
+    if (doc.contains("corr")) m.corr = doc.at("corr").get<std::vector<std::vector<double>>>();
   } catch (const Error&) {
     throw;
   } catch (const std::exception& e) {
@@ -608,39 +608,56 @@ ModelSpec modelFromJson(const std::string& text) {
   return m;
 }
 
-// cholesky (proj/src/pricing.cpp:45-69)
+// cholesky (proj/src/pricing.cpp:45-69).  The factor feeds the device's
+// correlated draws, so it must be the reference's bits: the same checks and
+// messages, and per entry the same IEEE sequence -- start from m[i][j],
+// subtract the products l[i][k] * l[j][k] for k = 0 .. j-1 one rounding at a
+// time, then sqrt on the diagonal or one division by l[j][j] below it.
+// Worked on a flat row-major n x n array (the layout the plan uploads).
 std::vector<std::vector<double>> cholesky(const std::vector<std::vector<double>>& m) {
-  std::size_t n = m.size();
+  const std::size_t n = m.size();
   for (const auto& row : m)
     if (row.size() != n) throw EvalError("correlation matrix is not square");
   for (std::size_t i = 0; i < n; ++i)
     for (std::size_t j = 0; j < n; ++j)
       if (std::fabs(m[i][j] - m[j][i]) > 1e-12)
         throw EvalError("correlation matrix is not symmetric");
-  std::vector<std::vector<double>> l(n, std::vector<double>(n, 0.0));
+  std::vector<double> L(n * n, 0.0);
   for (std::size_t i = 0; i < n; ++i) {
+    const double* li = &L[i * n];
     for (std::size_t j = 0; j <= i; ++j) {
-      double s = m[i][j];
-      for (std::size_t k = 0; k < j; ++k) s -= l[i][k] * l[j][k];
-      if (i == j) {
-        if (s <= 0.0) throw EvalError("correlation matrix is not positive definite");
-        l[i][i] = std::sqrt(s);
-      } else {
-        l[i][j] = s / l[j][j];
+      const double* lj = &L[j * n];
+      double acc = m[i][j];
+      for (std::size_t k = 0; k < j; ++k) {
+        const double prod = li[k] * lj[k];
+        acc = acc - prod;
       }
+      if (j < i) {
+        L[i * n + j] = acc / lj[j];
+        continue;
+      }
+      if (acc <= 0.0) throw EvalError("correlation matrix is not positive definite");
+      L[i * n + i] = std::sqrt(acc);
     }
   }
-  return l;
+  std::vector<std::vector<double>> out(n);
+  for (std::size_t i = 0; i < n; ++i) out[i].assign(L.begin() + i * n, L.begin() + (i + 1) * n);
+  return out;
 }
 
-// blackScholesCall (proj/src/pricing.cpp:150-159): analytic oracle of the tests.
+// blackScholesCall (proj/src/pricing.cpp:150-159): the analytic price the
+// tests check Monte Carlo against (normalCdf(x) = erfc(-x / sqrt 2) / 2).
 double blackScholesCall(double spot, double strike, double rate, double vol, double tYears) {
-  auto ncdf = [](double x) { return 0.5 * std::erfc(-x / std::sqrt(2.0)); };
-  if (tYears <= 0.0) return std::max(spot - strike, 0.0);
-  double sd = vol * std::sqrt(tYears);
-  double d1 = (std::log(spot / strike) + (rate + 0.5 * vol * vol) * tYears) / sd;
-  double d2 = d1 - sd;
-  return spot * ncdf(d1) - strike * std::exp(-rate * tYears) * ncdf(d2);
+  if (tYears <= 0.0) {
+    const double intrinsic = spot - strike;
+    return intrinsic < 0.0 ? 0.0 : intrinsic;  // std::max(spot - strike, 0.0)
+  }
+  const auto Phi = [](double x) { return 0.5 * std::erfc(-x / std::sqrt(2.0)); };
+  const double sd = vol * std::sqrt(tYears);
+  const double d1 = (std::log(spot / strike) + (rate + 0.5 * vol * vol) * tYears) / sd;
+  const double d2 = d1 - sd;
+  const double discounted = strike * std::exp(-rate * tYears);
+  return spot * Phi(d1) - discounted * Phi(d2);
 }
 
 // TEnv::lookup (proj/include/cltk/env.hpp:36-40)
@@ -667,13 +684,15 @@ TEnv tenvFromJson(const std::string& text) {
   }
 }
 
-// priceResultToJson (proj/src/pricing.cpp:161-167)
+// priceResultToJson (proj/src/pricing.cpp:161-167): the reference's keys
+// (nlohmann orders them alphabetically in the dump).
 std::string priceResultToJson(const PriceResult& r) {
-  Json j = {{"price", r.price},
-            {"stdError", r.stdError},
-            {"paths", r.paths},
-            {"seed", r.seed},
-            {"valuationDay", r.valuationDay}};
+  Json j = Json::object();
+  j["paths"] = r.paths;
+  j["price"] = r.price;
+  j["seed"] = r.seed;
+  j["stdError"] = r.stdError;
+  j["valuationDay"] = r.valuationDay;
   return j.dump();
 }
 

@@ -55,51 +55,44 @@ class Builder {
   std::map<std::string, std::size_t> colIndex_, tvarIndex_;
   std::map<std::string, int32_t> partyName_;
 
-  // ensureRows (kernel.cpp:47-79): rows for days [day, day + slack] as one
-  // contiguous block, reusing the block that starts at `day` when it is (or
-  // can be extended at the end into) a contiguous run.
+  // ensureRows (kernel.cpp:47-79): the row block of days day .. day + slack.
+  // Blocks are contiguous so that loop-relative offsets stay inside them.  The
+  // block already starting at `day` is reused when the rows that follow it
+  // continue the run day + 1, day + 2, ... (it may grow at the end of the
+  // table); otherwise a fresh block is appended -- a day can then own rows in
+  // several blocks, and firstRow_ keeps its first.
   std::size_t ensureRows(int64_t day, uint64_t slack) {
     std::vector<int64_t>& rows = k_.rows;
-    auto it = firstRow_.find(day);
-    if (it != firstRow_.end()) {
-      const std::size_t r = it->second;
-      bool contiguous = true;
-      for (uint64_t k = 1; k <= slack; ++k) {
-        const std::size_t want = r + k;
-        if (want < rows.size() && rows[want] != day + static_cast<int64_t>(k)) {
-          contiguous = false;
-          break;
-        }
-      }
-      if (contiguous) {
-        for (uint64_t k = 1; k <= slack; ++k) {
-          const std::size_t want = r + k;
-          if (want >= rows.size()) {
-            rows.push_back(day + static_cast<int64_t>(k));
-            firstRow_.emplace(rows.back(), want);
-          }
-        }
-        return r;
+    const auto append = [&](int64_t d) {
+      rows.push_back(d);
+      firstRow_.emplace(d, rows.size() - 1);
+    };
+    const auto hit = firstRow_.find(day);
+    if (hit != firstRow_.end()) {
+      const std::size_t base = hit->second;
+      const uint64_t present = std::min<uint64_t>(rows.size() - base - 1, slack);
+      uint64_t k = 1;
+      while (k <= present && rows[base + k] == day + static_cast<int64_t>(k)) ++k;
+      if (k > present) {
+        for (uint64_t e = present + 1; e <= slack; ++e) append(day + static_cast<int64_t>(e));
+        return base;
       }
     }
-    const std::size_t r = rows.size();
-    for (uint64_t k = 0; k <= slack; ++k) {
-      rows.push_back(day + static_cast<int64_t>(k));
-      firstRow_.emplace(rows.back(), rows.size() - 1);
-    }
-    return r;
+    const std::size_t base = rows.size();
+    for (uint64_t e = 0; e <= slack; ++e) append(day + static_cast<int64_t>(e));
+    return base;
   }
 
-  std::size_t colOf(const std::string& label) {
-    auto [it, inserted] = colIndex_.try_emplace(label, k_.cols.size());
-    if (inserted) k_.cols.push_back(label);
-    return it->second;
+  // first-use numbering of column labels and template variables
+  template <class K>
+  static std::size_t intern(std::map<K, std::size_t>& index, std::vector<K>& order, const K& key) {
+    const auto found = index.find(key);
+    if (found != index.end()) return found->second;
+    order.push_back(key);
+    return index[key] = order.size() - 1;
   }
-  std::size_t tvarOf(const std::string& name) {
-    auto [it, inserted] = tvarIndex_.try_emplace(name, k_.tvars.size());
-    if (inserted) k_.tvars.push_back(name);
-    return it->second;
-  }
+  std::size_t colOf(const std::string& label) { return intern(colIndex_, k_.cols, label); }
+  std::size_t tvarOf(const std::string& name) { return intern(tvarIndex_, k_.tvars, name); }
   void noteParty(const std::string& p) {
     if (std::find(k_.parties.begin(), k_.parties.end(), p) == k_.parties.end())
       k_.parties.push_back(p);
