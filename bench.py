@@ -87,7 +87,8 @@ def batch_literals(kern_json: str, workload: str = "brc_batch"):
             sub[0.75] = b
             sub[1.0] = r
         rows.append([sub.get(v, v) for v in base])
-    return rows
+    import numpy as np
+    return np.asarray(rows, dtype=np.float64)  # the host table a caller hands in
 
 
 WORKLOADS = {
@@ -277,7 +278,7 @@ def main():
     seed = 42
     literals = (batch_literals(kern_json, args.workload) if args.workload.endswith("_batch")
                 else None)
-    n_inst = len(literals) if literals else 1
+    n_inst = len(literals) if literals is not None else 1
     pricer = DistributedPricer(kern, model_json, [0], device=local, literals=literals, rng=args.rng,
                                jit=args.jit)
     info = pricer.plan.info
