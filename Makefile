@@ -43,10 +43,10 @@ $(OBJ)/jit_sources.o: $(OBJ)/jit_sources.cpp
 	$(HOSTCXX) $(CXXFLAGS) -c $< -o $@
 
 # three translation units compiled in parallel (mc_engine.cu CLTK_AOT_PART)
-$(OBJ)/mc_engine%.o: $(SRC)/mc_engine%.cu $(SRC)/mc_engine.cu $(HDRS) $(SRC)/engine_device.cuh
+$(CU_OBJS): $(OBJ)/%.o: $(SRC)/%.cu $(SRC)/mc_engine.cu $(HDRS)
 	@mkdir -p $(OBJ)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/mc_engine$*.ptxas.txt || (cat $(OBJ)/mc_engine$*.ptxas.txt; false)
-	@grep -E "Used|spill" $(OBJ)/mc_engine$*.ptxas.txt | head -40
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/$*.ptxas.txt || (cat $(OBJ)/$*.ptxas.txt; false)
+	@grep -E "Used|spill" $(OBJ)/$*.ptxas.txt | head -40
 
 $(LIB): $(HOST_OBJS) $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -cudart static -o $@ $^ -ldl

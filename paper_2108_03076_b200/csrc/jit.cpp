@@ -93,6 +93,7 @@ const std::vector<std::string>& nvrtcOptions() {
   static const std::vector<std::string> o = {"-arch=sm_100a", "-std=c++17", "-fmad=false",
                                              "-lineinfo", "-DCLTK_JIT=1",
                                              "-DCLTK_BLOCK=" + std::to_string(kBlock),
+                                             "-DCLTK_MAX_BATCH=" + std::to_string(CLTK_MAX_BATCH),
                                              "-DCLTK_MAX_ASSETS=" + std::to_string(CLTK_MAX_ASSETS)};
   return o;
 }
