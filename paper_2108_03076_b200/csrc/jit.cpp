@@ -262,6 +262,10 @@ struct Gen {
   // registers are always stored as values.
   bool logMode = false;
   std::set<uint32_t> noLog;
+  // registers a step class stores as values although they are log-domain
+  // there: the last writer of a running extremum that the outputs or the
+  // instance section read (exp once per path instead of once per step)
+  std::map<uint32_t, std::set<uint32_t>> exitValue;
   std::map<uint32_t, std::map<uint32_t, int>> entryDom;  // class -> register -> 1 if log
 
   struct Val {
@@ -380,7 +384,9 @@ struct Gen {
       for (uint32_t r : dirty) (*final)[r] = cur[r].val.empty() ? cur[r].log : cur[r].val;
       return exitDom;
     }
+    const auto ev = exitValue.find(block);
     for (uint32_t r : dirty) {
+      if (ev != exitValue.end() && ev->second.count(r) && cur[r].val.empty()) value(r);
       const Val& x = cur[r];
       const bool isLog = x.val.empty();
       exitDom[r] = isLog ? 1 : 0;
@@ -486,9 +492,11 @@ std::string jitSource(CompiledProgram& prog) {
     if (o.err != CLTK_NO_ERR && o.err < h.n_thread) g.outRead.insert(o.err);
   }
   // Log-domain spots: find each step class's entry domains by running the
-  // step sequence; a register seen in two domains at one class's entry, or
-  // still log-domain when the outputs / the instance section read it, is
-  // stored as a value everywhere (noLog) and the sequence is re-run.
+  // step sequence.  A register still log-domain when the outputs / the
+  // instance section read it is first stored as a value by the class that
+  // last writes it (exitValue); a register seen in two domains at one class's
+  // entry (or whose exit conversion caused that) is stored as a value
+  // everywhere (noLog); the sequence is re-run after each change.
   g.logMode = g.sRegs && std::getenv("CLTK_JIT_NO_LOGSPOTS") == nullptr;
   if (g.logMode) {
     std::vector<std::set<uint32_t>> firstReads(classOps.size());
@@ -496,11 +504,14 @@ std::string jitSource(CompiledProgram& prog) {
       firstReads[c] = Gen::readsFirst(classOps[c], h.n_thread);
     std::set<uint32_t> endReads(g.outRead);
     for (uint32_t r : Gen::readsFirst(instOps, h.n_thread)) endReads.insert(r);
+    std::set<uint32_t> triedExit;
     for (;;) {
       g.entryDom.clear();
       std::map<uint32_t, std::map<uint32_t, int>> exitDom;  // per class, fixed entries
       std::map<uint32_t, int> dom;
+      std::map<uint32_t, uint32_t> lastWriter;  // register -> class that wrote it last
       uint32_t bad = ~0u;
+      bool atEnd = false;
       for (const cltk_step& st : prog.steps) {
         const uint32_t c = st.jit_class;
         if (c == 0) continue;
@@ -516,12 +527,24 @@ std::string jitSource(CompiledProgram& prog) {
           std::ostringstream dry;
           exitDom[c] = g.emit(dry, classOps[c], true, c, "");
         }
-        for (const auto& kv : exitDom[c]) dom[kv.first] = kv.second;
+        for (const auto& kv : exitDom[c]) {
+          dom[kv.first] = kv.second;
+          lastWriter[kv.first] = c;
+        }
       }
       if (bad == ~0u)
         for (uint32_t r : endReads)
-          if (dom.count(r) && dom[r]) bad = r;
+          if (dom.count(r) && dom[r]) {
+            bad = r;
+            atEnd = true;
+          }
       if (bad == ~0u) break;
+      if (atEnd && !triedExit.count(bad) && lastWriter.count(bad)) {
+        g.exitValue[lastWriter[bad]].insert(bad);
+        triedExit.insert(bad);
+        continue;
+      }
+      for (auto& kv : g.exitValue) kv.second.erase(bad);
       g.noLog.insert(bad);
     }
   }
