@@ -163,6 +163,51 @@ def test_up_barrier_source_uses_log_fmax():
     assert ("log_fmax(" in src or "log_fmax_b(" in src) and "kLogSpots = true" in src
 
 
+def _brc_batch_literals(n=64):
+    """n instances of the BRC template: knock-in barrier 50..80 % of spot."""
+    import numpy as np
+    kj = load_kernel("brc")
+    base = E.kernel_literals(kj)
+    spots = {3758.05: 2630.635, 11840.0: 8288.0, 1200.0: 840.0}
+    rows = []
+    for i in range(n):
+        b = 0.5 + 0.3 * i / (n - 1)
+        sub = {bar: sp * b for sp, bar in spots.items()}
+        rows.append([sub.get(v, v) for v in base])
+    return kj, np.asarray(rows)
+
+
+def test_template_batch_minima_stay_log_domain_until_the_last_step():
+    """C4 BRC batch: the knock-in minima are compared with per-instance
+    barriers in the instance section, so they must reach it as spots.  They
+    stay logarithms through the 365 running-minimum steps (log_fmin, no exp
+    per step) and the last step exponentiates each one once."""
+    kj, lit = _brc_batch_literals()
+    src = E.jit_source(E.Kernel(kj), load_model("three"), [0], literals=lit)
+    cases = re.split(r"case \d+: \{", src.split("static __device__ __forceinline__ void inst(")[0])[1:]
+    assert len(cases) == 3
+    mins = [c for c in cases if "log_fmin" in c]
+    assert len(mins) == 2, "running-min classes in the log domain"
+    running, last = (mins[0], mins[1]) if mins[0].count("spot_exp") < mins[1].count("spot_exp") else (mins[1], mins[0])
+    assert "spot_exp" not in running  # 365 steps without an exp
+    assert last.count("spot_exp") == 6  # three minima + the three final spots, once each
+
+
+@pytest.mark.gpu
+def test_template_batch_log_domain_minima_bitwise():
+    """The same batch priced with the NVRTC kernel (log-domain minima,
+    exponentiated at the last step) and the interpreter (spot-domain minima):
+    bit-identical instance prices."""
+    kj, lit = _brc_batch_literals(40)
+    m = load_model("three")
+    a = E.price_template(kj, lit, m, 30000, 11, jit=False)
+    b = E.price_template(kj, lit, m, 30000, 11, jit=True)
+    assert len(a) == len(b) == 40
+    for ra, rb in zip(a, b):
+        x, y = ra[0], rb[0]
+        assert x["price"] == y["price"] and x["std_error"] == y["std_error"], (x, y)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", ["down", "up"])
 def test_log_domain_extrema_bitwise_vs_interpreter(variant):
