@@ -1235,6 +1235,31 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
         ok = std::isfinite(cum) && cum < 500.0;
       }
       h.log_bounded = ok ? 1u : 0u;
+    } else if (plan.rng == CLTK_RNG_SOBOL && !plan.bridge.empty()) {
+      // QMC: logS_j(t_s) = logS0_j + A_sj + B_sj * sum_l L_jl W_l(t_s) with
+      // |W_l(t_s)| bounded by running the bridge program on bounds
+      // (|W_m| <= wl |W_l| + wr |W_r| + sd * zmax), zmax = 6.5 >
+      // |AS241((2^32 - 1 + 0.5) 2^-32)| (32-bit Sobol points, shifted or not)
+      std::vector<double> slotB(std::max<uint32_t>(1, plan.bridgeSlots), 0.0);
+      auto slotBound = [&](uint16_t sl) { return sl == CLTK_BR_ORIGIN ? 0.0 : slotB[sl]; };
+      bool ok = true;
+      for (const cltk_step& st : P.steps) {
+        if (st.draws != STEP_DRAW) continue;
+        for (uint32_t b = st.br_begin; b < st.br_end; ++b) {
+          const cltk_bridge_op& op = plan.bridge[b];
+          slotB[op.dst] = std::fabs(op.wl) * slotBound(op.l) + std::fabs(op.wr) * slotBound(op.r) +
+                          std::fabs(op.sd) * 6.5;
+        }
+        const double bw = slotB[st.br_emit];
+        for (uint32_t j = 0; j < nA && ok; ++j) {
+          double lsum = 0.0;
+          for (uint32_t l = 0; l <= j; ++l) lsum += std::fabs(plan.chol[j * CLTK_MAX_ASSETS + l]);
+          const double m = std::fabs(plan.logS0[j]) + std::fabs(st.A[j]) + std::fabs(st.B[j]) * lsum * bw;
+          ok = std::isfinite(m) && m < 500.0;
+        }
+        if (!ok) break;
+      }
+      h.log_bounded = ok ? 1u : 0u;
     }
     h.first_draw = nSteps;
     for (uint32_t s0 = 0; s0 < nSteps; ++s0)

@@ -163,6 +163,21 @@ def test_up_barrier_source_uses_log_fmax():
     assert ("log_fmax(" in src or "log_fmax_b(" in src) and "kLogSpots = true" in src
 
 
+def test_qmc_log_spots_bounded_by_the_bridge():
+    """QMC plans get the range-check-free log-domain ops too: the host bounds
+    every log-spot by running the bridge program on |W| bounds (AS241 of
+    32-bit Sobol points: |z| < 6.5)."""
+    src = E.jit_source(E.Kernel(load_kernel("brc")), load_model("three"), [0], rng="sobol")
+    assert "log_fmin_b(" in src and "log_fmin(" not in src
+    # a model whose log-spots can leave (-500, 500) keeps the checked forms
+    import copy
+    wild = copy.deepcopy(load_model("three"))
+    for v in wild["labels"].values():
+        v["vol"] = 40.0
+    src = E.jit_source(E.Kernel(load_kernel("brc")), wild, [0], rng="sobol")
+    assert "log_fmin(" in src and "log_fmin_b(" not in src
+
+
 def _brc_batch_literals(n=64):
     """n instances of the BRC template: knock-in barrier 50..80 % of spot."""
     import numpy as np
