@@ -21,6 +21,12 @@
 #include "jit.hpp"
 #include "nccl_comm.hpp"
 
+// simulate_qmc (engine_device.cuh) reads the step header as two 16-byte words
+static_assert(offsetof(cltk_step_hdr, draws) == 0 && offsetof(cltk_step_hdr, br_begin) == 12 &&
+                  offsetof(cltk_step_hdr, br_end) == 16 && offsetof(cltk_step_hdr, br_emit) == 20 &&
+                  sizeof(cltk_step_hdr) == 32,
+              "step header layout");
+
 namespace cltk {
 namespace b200 {
 
