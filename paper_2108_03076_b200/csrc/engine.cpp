@@ -254,6 +254,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   // jitSource rewrites the header's register window and the steps' classes:
   // JIT_AUTO keeps the interpreter's copy in case NVRTC or the module load fails
   std::vector<cltk_step> interpSteps;
+  std::vector<double> interpInst;  // (jitSource may append reciprocal literal columns)
   cltk_plan_header interpHdr{};
   // models of more than CLTK_AOT_MAX_ASSETS assets have no ahead-of-time kernel
   const bool bigModel = I.prog.header.n_assets > CLTK_AOT_MAX_ASSETS;
@@ -267,6 +268,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
     if (!use && (opt.jit == JIT_ON || bigModel)) throw UnsupportedError("jit: " + why);
     if (use) {
       interpSteps = I.prog.steps;
+      interpInst = I.prog.instConst;
       interpHdr = I.prog.header;
       try {
         jitSrc = jitSource(I.prog);  // assigns steps[].jit_class (uploaded below)
@@ -274,6 +276,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
         if (opt.jit == JIT_ON || bigModel) throw;
         jitSrc.clear();
         I.prog.steps = interpSteps;
+        I.prog.instConst = interpInst;
         I.prog.header = interpHdr;
       }
     }
@@ -292,6 +295,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
       jitSrc.clear();
       I.jitFn = nullptr;
       I.prog.steps = interpSteps;
+      I.prog.instConst = interpInst;
       I.prog.header = interpHdr;
     }
   }

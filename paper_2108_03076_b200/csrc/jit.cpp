@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <unistd.h>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <filesystem>
 #include <map>
@@ -270,7 +271,23 @@ struct Gen {
 
   struct Val {
     std::string log, val;  // log form (log-domain value) and/or value form
+    bool spot = false;     // the value is a spot: exp of a bounded log-spot (> 0, in
+                           // [2^-722, 2^722]) or a min / max / select of such
   };
+
+  // Divisions by instance literals in the instance-major section (inst_t):
+  // a spot divided by a literal whose every instance value lies in
+  // [2^-100, 2^100] is rounded from the literal's host-computed reciprocal
+  // RN(1/b) (an extra instance-literal column) in three operations --
+  // q = RN(a y), r = a - b q (exact), RN(q + r y) = RN(a/b) (Markstein's
+  // theorem; operands and quotient far from over/underflow) -- instead of a
+  // full IEEE division per (path, instance).
+  bool spotOK = false;                // spots are exps of bounded log-spots
+  std::set<uint32_t> spotRegs;        // registers that hold spots whenever read
+  std::set<uint32_t> recipOK;         // instance-literal columns usable as divisors
+  uint32_t niCols = 0;                // instance-literal columns before the reciprocals
+  mutable std::map<uint32_t, uint32_t> recipCol;     // literal column -> reciprocal column
+  mutable std::map<uint32_t, int>* storeRec = nullptr;  // analysis: register -> all stores spot
 
   // Straight-line emission of one block with its values in locals: a register
   // is loaded from its shared-memory column at its first read in the block (if
@@ -305,7 +322,7 @@ struct Gen {
     auto fresh = [&]() { return "v" + std::to_string(n++); };
     auto operand = [&](uint32_t i) -> Val {
       if (i < nA && inStep && sRegs) {
-        if (!lm) return Val{"", "S[" + std::to_string(i) + "]"};
+        if (!lm) return Val{"", "S[" + std::to_string(i) + "]", prog.header.log_bounded != 0};
         auto it = slotVal.find(i);
         if (it != slotVal.end()) return it->second;
         return slotVal[i] = Val{"L[" + std::to_string(i) + "]", ""};
@@ -337,7 +354,7 @@ struct Gen {
         src = "JC(" + std::to_string(i) + ")";
       }
       os << ind << "const double " << v << " = " << src << ";\n";
-      return cur[i] = isLog ? Val{v, ""} : Val{"", v};
+      return cur[i] = isLog ? Val{v, ""} : Val{"", v, i < nThread && spotRegs.count(i) > 0};
     };
     // the value form of operand i (exp of a log-domain value, formed once)
     auto value = [&](uint32_t i) -> std::string {
@@ -347,6 +364,7 @@ struct Gen {
       os << ind << "const double " << v << " = " << (prog.header.log_bounded ? "spot_exp_b(" : "spot_exp(")
          << x.log << ");\n";
       x.val = v;
+      x.spot = spotOK;
       if (i < nA && inStep && sRegs) slotVal[i] = x;
       else cur[i] = x;
       return v;
@@ -369,11 +387,24 @@ struct Gen {
         const std::string a = value(o.a);
         const std::string b = usesB(o.op) ? value(o.b) : std::string();
         const std::string c = o.op == OP_SEL ? value(o.c) : std::string();
+        const bool sa = operand(o.a).spot, sb = usesB(o.op) && operand(o.b).spot,
+                   sc = o.op == OP_SEL && operand(o.c).spot;
+        const uint32_t lit0 = nThread + nc;
+        std::string expr = opExpr(o);
+        if (final && spotOK && o.op == OP_DIV && sa && o.b >= lit0 && o.b < lit0 + ni &&
+            recipOK.count(o.b - lit0)) {
+          auto rc = recipCol.find(o.b - lit0);
+          if (rc == recipCol.end())
+            rc = recipCol.emplace(o.b - lit0, niCols + static_cast<uint32_t>(recipCol.size())).first;
+          expr = "div_recip(a, b, JI(" + std::to_string(rc->second) + "))";
+        }
         os << ind << "double " << t << ";\n" << ind << "{ const double a = " << a << ";";
         if (!b.empty()) os << " const double b = " << b << ";";
         if (!c.empty()) os << " const double c = " << c << ";";
-        os << " " << t << " = " << opExpr(o) << "; }\n";
+        os << " " << t << " = " << expr << "; }\n";
         res = Val{"", t};
+        if ((o.op == OP_MIN || o.op == OP_MAX) && sa && sb) res.spot = true;
+        if (o.op == OP_SEL && sb && sc) res.spot = true;
       }
       cur[o.d] = res;
       if (!res.log.empty() && noLog.count(o.d)) value(o.d);  // stored as a value
@@ -396,6 +427,12 @@ struct Gen {
         for (uint32_t bl : it->second)
           if (bl != block) live = true;
       if (live) os << ind << "JW(" << r << ", " << (isLog ? x.log : x.val) << ");\n";
+      if (live && storeRec) {
+        const int sp = (isLog || x.spot) ? 1 : 0;  // a log-domain store reads back as a spot
+        auto it = storeRec->find(r);
+        if (it == storeRec->end()) storeRec->emplace(r, sp);
+        else it->second = std::min(it->second, sp);
+      }
     }
     return exitDom;
   }
@@ -548,6 +585,42 @@ std::string jitSource(CompiledProgram& prog) {
       g.noLog.insert(bad);
     }
   }
+  // Spot registers (for the instance section's reciprocal divisions): start
+  // from every thread register and keep those whose every store in the step
+  // classes is a spot or a log-spot, to a fixed point.
+  g.spotOK = g.logMode && h.log_bounded != 0;
+  g.niCols = h.n_inst_const;
+  if (g.spotOK && h.inst_major && h.n_inst_const) {
+    for (uint32_t r = h.n_assets; r < h.n_thread; ++r) g.spotRegs.insert(r);
+    for (;;) {
+      std::map<uint32_t, int> rec;
+      g.storeRec = &rec;
+      for (size_t c = 1; c < classOps.size(); ++c) {
+        std::ostringstream dry;
+        g.emit(dry, classOps[c], true, static_cast<uint32_t>(c), "");
+      }
+      g.storeRec = nullptr;
+      std::set<uint32_t> next;
+      for (uint32_t r : g.spotRegs) {
+        const auto it = rec.find(r);
+        if (it != rec.end() && it->second) next.insert(r);
+      }
+      if (next == g.spotRegs) break;
+      g.spotRegs.swap(next);
+    }
+    // literal columns whose every instance value is a safe divisor
+    const size_t nInst = h.n_instances, ni = h.n_inst_const;
+    for (uint32_t k = 0; k < ni; ++k) {
+      bool ok = prog.instConst.size() >= nInst * ni;
+      for (size_t i = 0; i < nInst && ok; ++i) {
+        const double v = prog.instConst[i * ni + k];
+        ok = std::isfinite(v) && v >= 0x1.0p-100 && v <= 0x1.0p+100;
+      }
+      if (ok) g.recipOK.insert(k);
+    }
+  } else {
+    g.spotOK = false;
+  }
   std::ostringstream os;
   os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
         "#define CLTK_JIT 1\n"
@@ -639,6 +712,18 @@ std::string jitSource(CompiledProgram& prog) {
      << (prog.faultBuild ? "true" : "false")
      << ", " << (h.reg_acc ? 1 : 0) << ", " << (h.stream ? 1 : 0) << ", "
      << (h.inst_major ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
+  // the reciprocal columns the instance section divides by: RN(1/b) per
+  // instance, computed here (IEEE division on the host)
+  if (!g.recipCol.empty()) {
+    const size_t nInst = h.n_instances, ni = g.niCols, nn = ni + g.recipCol.size();
+    std::vector<double> t(nInst * nn);
+    for (size_t i = 0; i < nInst; ++i) {
+      for (size_t k = 0; k < ni; ++k) t[i * nn + k] = prog.instConst[i * ni + k];
+      for (const auto& kv : g.recipCol) t[i * nn + kv.second] = 1.0 / prog.instConst[i * ni + kv.first];
+    }
+    prog.instConst.swap(t);
+    prog.header.n_inst_const = static_cast<uint32_t>(nn);
+  }
   // Shared-memory register columns: only the registers the generated code
   // stores or loads (JW / JR) or the outputs read; the rest live in locals.
   std::string src = os.str();

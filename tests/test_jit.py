@@ -179,7 +179,8 @@ def test_qmc_log_spots_bounded_by_the_bridge():
 
 
 def _brc_batch_literals(n=64):
-    """n instances of the BRC template: knock-in barrier 50..80 % of spot."""
+    """n instances of the BRC template: knock-in barrier 50..80 % of spot,
+    strike (initial fixing) 90..110 % of spot."""
     import numpy as np
     kj = load_kernel("brc")
     base = E.kernel_literals(kj)
@@ -187,7 +188,9 @@ def _brc_batch_literals(n=64):
     rows = []
     for i in range(n):
         b = 0.5 + 0.3 * i / (n - 1)
+        r = 0.9 + 0.2 * ((i * 7) % n) / (n - 1)
         sub = {bar: sp * b for sp, bar in spots.items()}
+        sub.update({sp: sp * r for sp in spots})
         rows.append([sub.get(v, v) for v in base])
     return kj, np.asarray(rows)
 
@@ -206,6 +209,29 @@ def test_template_batch_minima_stay_log_domain_until_the_last_step():
     running, last = (mins[0], mins[1]) if mins[0].count("spot_exp") < mins[1].count("spot_exp") else (mins[1], mins[0])
     assert "spot_exp" not in running  # 365 steps without an exp
     assert last.count("spot_exp") == 6  # three minima + the three final spots, once each
+
+
+def test_template_batch_divides_by_host_reciprocals():
+    """The instance-major section divides each spot by the instance's literal
+    through RN(1/literal) from extra literal columns (3 FP64 operations,
+    Markstein's exact rounding) -- only while every instance value of that
+    literal lies in [2^-100, 2^100]; otherwise the full IEEE division stays."""
+    kj, lit = _brc_batch_literals()
+    m = load_model("three")
+    src = E.jit_source(E.Kernel(kj), m, [0], literals=lit)
+    inst_t = src.split("inst_t(")[1]
+    assert inst_t.count("div_recip(") == 3 and "__ddiv_rn" not in inst_t
+    recip = [int(c) for c in re.findall(r"div_recip\(a, b, JI\((\d+)\)\)", inst_t)]
+    plain = [int(c) for c in re.findall(r"= JI\((\d+)\);", src)]
+    assert len(set(recip)) == 3 and min(recip) > max(plain)  # appended columns
+    bad = lit.copy()
+    base = list(E.kernel_literals(kj))
+    for c, v in enumerate(base):  # one instance's first-asset fixing out of range
+        if v == 3758.05:
+            bad[5, c] = 1e-40  # below 2^-100
+    src = E.jit_source(E.Kernel(kj), m, [0], literals=bad)
+    inst_t = src.split("inst_t(")[1]
+    assert inst_t.count("div_recip(") == 2 and inst_t.count("__ddiv_rn") == 1
 
 
 @pytest.mark.gpu
