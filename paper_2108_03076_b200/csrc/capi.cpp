@@ -430,8 +430,9 @@ int cltk_compile_listing(const char* const* kernel_jsons, size_t n_instances,
     CompileOptions co;
     co.rewrite = rewrite != 0;
     CompiledProgram P = compileProgram(ptrs, sp, std::vector<uint64_t>(days, days + n_days), co);
-    char* p = static_cast<char*>(std::malloc(P.listing.size() + 1));
-    std::memcpy(p, P.listing.c_str(), P.listing.size() + 1);
+    const std::string listing = programListing(P);
+    char* p = static_cast<char*>(std::malloc(listing.size() + 1));
+    std::memcpy(p, listing.c_str(), listing.size() + 1);
     *json = p;
   });
 }

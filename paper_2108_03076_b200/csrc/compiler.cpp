@@ -1285,7 +1285,17 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   P.nSharedOps = endBegin;
   P.nInstOps = static_cast<uint32_t>(linear.size()) - endBegin;
 
-  // ---- listing (tests / DESIGN.md)
+  // the listing (tests / DESIGN.md) is built on demand: programListing()
+  P.stepCodeBegin = stepBegin;
+  P.days = plan.days;
+  return P;
+}
+
+std::string programListing(const CompiledProgram& P) {
+  const cltk_plan_header& h = P.header;
+  const uint32_t nA = h.n_assets, nThread = h.n_thread, nInstC = h.n_inst_const;
+  const uint32_t nInst = h.n_instances, endBegin = P.nSharedOps;
+  const std::vector<uint32_t>& stepBegin = P.stepCodeBegin;
   Json L;
   Json ops = Json::array();
   for (std::size_t t = 0; t < P.code.size(); ++t) {
@@ -1307,11 +1317,11 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
                   {"A", A}, {"B", Bv}, {"S", Sv}, {"br", {s.br_begin, s.br_end, s.br_emit}}});
   }
   L["steps"] = st;
-  L["days"] = plan.days;
-  L["rng"] = plan.rng;
-  L["bridge_slots"] = plan.bridgeSlots;
+  L["days"] = P.days;
+  L["rng"] = h.rng;
+  L["bridge_slots"] = h.n_bridge_slots;
   Json br = Json::array();
-  for (const auto& b : plan.bridge)
+  for (const auto& b : P.bridge)
     br.push_back({b.node, b.dst, b.l == CLTK_BR_ORIGIN ? -1 : (int)b.l,
                   b.r == CLTK_BR_ORIGIN ? -1 : (int)b.r, b.wl, b.wr, b.sd});
   L["bridge"] = br;
@@ -1330,7 +1340,7 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   L["n_shared_const"] = h.n_shared_const;
   L["n_inst_const"] = nInstC;
   L["n_instances"] = nInst;
-  L["inst_code"] = {endBegin, static_cast<uint32_t>(linear.size())};
+  L["inst_code"] = {endBegin, endBegin + P.nInstOps};
   L["packed_words"] = P.packed.size();
   L["kernel_nodes"] = P.kernelNodes;
   L["dag_nodes"] = P.dagNodes;
@@ -1341,8 +1351,7 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
   for (uint32_t j = 0; j < nA; ++j) ls.push_back(h.logS0[j]);
   L["logS0"] = ls;
   L["vt"] = {vtName(VT::R), vtName(VT::B), vtName(VT::I), vtName(VT::E)};
-  P.listing = L.dump();
-  return P;
+  return L.dump();
 }
 
 }  // namespace b200

@@ -66,7 +66,8 @@ struct CompiledProgram {
   cltk_plan_header header{};
   uint64_t kernelNodes = 0, dagNodes = 0;
   uint32_t nSharedOps = 0, nInstOps = 0;
-  std::string listing;                 // JSON dump
+  std::vector<uint32_t> stepCodeBegin; // per step, the start of its ops in `code` (+ end)
+  std::vector<int64_t> days;           // valuation days
   bool faultBuild = false;             // test build: RunArgs fault injection compiled in
 };
 
@@ -96,6 +97,9 @@ LiteralTable literalTableFromInstances(const std::vector<const Kernel*>& instanc
 
 CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const SimPlanHost& plan,
                                const std::vector<uint64_t>& days, const CompileOptions& opt);
+// The program as JSON (ops, steps, constants, outputs, header fields): tests,
+// DESIGN.md, the bench's upload accounting.
+std::string programListing(const CompiledProgram& P);
 CompiledProgram compileProgram(const std::vector<const Kernel*>& instances,
                                const SimPlanHost& plan, const std::vector<uint64_t>& days,
                                const CompileOptions& opt);

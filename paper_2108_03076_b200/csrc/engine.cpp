@@ -526,7 +526,7 @@ std::vector<PriceResult> Plan::finalize(uint64_t paths, uint64_t seed, const voi
   return out;
 }
 
-std::string Plan::dump() const { return impl_->prog.listing; }
+std::string Plan::dump() const { return programListing(impl_->prog); }
 
 void Plan::setFault(uint64_t path, uint32_t draw) {
   if (!impl_->fault) throw UnsupportedError("fault injection: plan not built with fault_inject");
