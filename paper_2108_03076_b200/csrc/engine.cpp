@@ -146,6 +146,7 @@ const SobolTables& sobolTables(int dev) {
   ck(cudaMemcpy(static_cast<uint32_t*>(p) + V.size(), T5.data(), T5.size() * sizeof(uint32_t),
                 cudaMemcpyHostToDevice),
      "H2D");
+  ck(cudaStreamSynchronize(0), "cudaStreamSynchronize");  // (pageable copies: DMA landed)
   SobolTables t{static_cast<const uint32_t*>(p), static_cast<const uint32_t*>(p) + V.size()};
   return tabs.emplace(dev, t).first->second;
 }
@@ -321,6 +322,9 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
     I.owned.push_back(base);
     ck(cudaMemcpy(base, st.bytes.data(), st.bytes.size(), cudaMemcpyHostToDevice),
        "cudaMemcpy H2D");
+    // a pageable-memory cudaMemcpy may return before its DMA lands; the plan's
+    // launches run on other (non-blocking) streams, which do not wait for it
+    ck(cudaStreamSynchronize(0), "cudaStreamSynchronize");
     auto at = [&](size_t o, bool nonEmpty) { return nonEmpty ? base + o : nullptr; };
     I.dev.steps = reinterpret_cast<const unsigned char*>(at(oSteps, !I.prog.steps.empty()));
     I.dev.code = reinterpret_cast<const uint64_t*>(at(oCode, !I.prog.packed.empty()));

@@ -265,6 +265,35 @@ def test_log_domain_extrema_bitwise_vs_interpreter(variant):
 
 
 @pytest.mark.gpu
+def test_qmc_multi_day_reduction_deterministic():
+    """Regression: QMC plans with several outputs park the per-path values in
+    rows counted from the normal scratch; the QMC P region (32-bit Sobol
+    integers) once took half a row for odd batch sizes, which put the parked
+    values in other threads' bridge-slot columns -- a race that changed
+    random chunks of the worst-off's three-day price from launch to launch.
+    Repeated launches must give one bit pattern, the interpreter's."""
+    from paper_2108_03076_b200.distributed import DistributedPricer
+    import torch
+    m = load_model("three")
+    stream = torch.cuda.current_stream(0).cuda_stream
+    paths = 1 << 20
+    ref = None
+    for jit in (False, True):
+        pr = DistributedPricer(E.Kernel(load_kernel("worst-off")), m, [0, 100, 300], device=0,
+                               rng="sobol", jit=jit)
+        _, nc = pr.plan.chunking(paths)
+        for _ in range(12 if jit else 1):
+            parts = pr.partials(paths)
+            parts.zero_()
+            pr.plan.launch(paths, 20, 0, nc, parts.data_ptr(), stream)
+            torch.cuda.synchronize()
+            bits = parts.view(torch.int64).clone()
+            if ref is None:
+                ref = bits
+            assert torch.equal(bits, ref)
+
+
+@pytest.mark.gpu
 def test_disk_cache_reuses_and_repairs_the_cubin(tmp_path):
     """The NVRTC cubin of a program is written to CLTK_JIT_CACHE_DIR and loaded
     by a later process; a damaged entry is recompiled, never trusted."""
