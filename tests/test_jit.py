@@ -282,7 +282,7 @@ def test_qmc_multi_day_reduction_deterministic():
         pr = DistributedPricer(E.Kernel(load_kernel("worst-off")), m, [0, 100, 300], device=0,
                                rng="sobol", jit=jit)
         _, nc = pr.plan.chunking(paths)
-        for _ in range(12 if jit else 1):
+        for _ in range(12 if jit else 4):
             parts = pr.partials(paths)
             parts.zero_()
             pr.plan.launch(paths, 20, 0, nc, parts.data_ptr(), stream)
