@@ -12,9 +12,9 @@
  * 5 eval); err (may be NULL) receives the reference's message.  Device
  * failures return 4 with a "device: ..." message.
  *
- * Limits that differ from the reference: models of at most 16 assets
+ * Limits that differ from the reference: models of at most 32 assets
  * (CLTK_MAX_ASSETS; the reference has no cap, proj/src/pricing.cpp:217-245);
- * models of 9..16 assets run the NVRTC payoff kernel only (jit = 0 and the
+ * models of 9..32 assets run the NVRTC payoff kernel only (jit = 0 and the
  * QMC mode take at most 8) -- beyond that the call returns 4
  * (UnsupportedError).  At most 2^40 paths per call, and 2^32 in the QMC mode.  The pricing functions never change their inputs;
  * one plan (cltk_plan_*) serves one caller at a time, any number of plans

@@ -22,10 +22,11 @@
 #define CLTK_OP_BITS 8
 #define CLTK_FIELD_BITS 14
 #define CLTK_MAX_OPERANDS (1 << CLTK_FIELD_BITS)
-// Models of up to 16 assets; the ahead-of-time (interpreter) kernels and the
-// QMC mode cover up to CLTK_AOT_MAX_ASSETS, larger models run the NVRTC kernel.
+// Models of up to 32 assets (one step's draws fill a 32-bit draw window); the
+// ahead-of-time (interpreter) kernels and the QMC mode cover up to
+// CLTK_AOT_MAX_ASSETS, larger models run the NVRTC kernel.
 #ifndef CLTK_MAX_ASSETS
-#define CLTK_MAX_ASSETS 16
+#define CLTK_MAX_ASSETS 32
 #endif
 #define CLTK_AOT_MAX_ASSETS 8
 
