@@ -265,21 +265,25 @@ def test_log_domain_extrema_bitwise_vs_interpreter(variant):
 
 
 @pytest.mark.gpu
-def test_qmc_multi_day_reduction_deterministic():
-    """Regression: QMC plans with several outputs park the per-path values in
-    rows counted from the normal scratch; the QMC P region (32-bit Sobol
-    integers) once took half a row for odd batch sizes, which put the parked
-    values in other threads' bridge-slot columns -- a race that changed
-    random chunks of the worst-off's three-day price from launch to launch.
-    Repeated launches must give one bit pattern, the interpreter's."""
+@pytest.mark.parametrize("kern,model,days,paths", [("worst-off", "three", [0, 100, 300], 1 << 20),
+                                                   ("european-call", "call", [0, 30, 60],
+                                                    (1 << 22) + 64)])
+def test_qmc_multi_day_reduction_deterministic(kern, model, days, paths):
+    """Regression: QMC plans with several outputs park the per-path values
+    in the normal scratch.  Parked in rows counted from X they once landed in
+    other threads' data -- behind a half-row P region in other threads'
+    bridge slots (odd batch sizes, the worst-off), and inside P itself, whose
+    32-bit Sobol integers pack two threads per double (one-asset models, the
+    call) -- races that changed random chunks of multi-day QMC prices from
+    launch to launch.  QMC now parks in its bridge-slot rows.  Repeated
+    launches must give one bit pattern, the interpreter's."""
     from paper_2108_03076_b200.distributed import DistributedPricer
     import torch
-    m = load_model("three")
+    m = load_model(model)
     stream = torch.cuda.current_stream(0).cuda_stream
-    paths = 1 << 20
     ref = None
     for jit in (False, True):
-        pr = DistributedPricer(E.Kernel(load_kernel("worst-off")), m, [0, 100, 300], device=0,
+        pr = DistributedPricer(E.Kernel(load_kernel(kern)), m, days, device=0,
                                rng="sobol", jit=jit)
         _, nc = pr.plan.chunking(paths)
         for _ in range(12 if jit else 4):
