@@ -164,7 +164,7 @@ SimPlanHost buildSimPlan(const Kernel& k, const ModelSpec& model, uint32_t rng) 
                            " model assets, model has " + std::to_string(n));
   p.nAssets = static_cast<uint32_t>(n);
   for (std::size_t i = 0; i < n; ++i)
-    for (std::size_t j = 0; j < n; ++j) p.chol[i * CLTK_MAX_ASSETS + j] = chol[i][j];
+    for (std::size_t j = 0; j < n; ++j) p.chol[i * n + j] = chol[i][j];  // packed rows of n
   // Per-step constants, in the reference's operation order.
   std::vector<const AssetSpec*> spec(n);
   for (std::size_t j = 0; j < n; ++j) {
@@ -1228,7 +1228,7 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
       bool ok = true;
       for (uint32_t j = 0; j < nA && ok; ++j) {
         double lsum = 0.0;
-        for (uint32_t l = 0; l <= j; ++l) lsum += std::fabs(plan.chol[j * CLTK_MAX_ASSETS + l]);
+        for (uint32_t l = 0; l <= j; ++l) lsum += std::fabs(plan.chol[j * nA + l]);
         double cum = std::fabs(plan.logS0[j]);
         for (const cltk_step& st : P.steps)
           if (st.draws == STEP_DRAW) cum += std::fabs(st.A[j]) + std::fabs(st.B[j]) * lsum * 8.5;
@@ -1253,7 +1253,7 @@ CompiledProgram compileProgram(const Kernel& k, const LiteralTable& lits, const 
         const double bw = slotB[st.br_emit];
         for (uint32_t j = 0; j < nA && ok; ++j) {
           double lsum = 0.0;
-          for (uint32_t l = 0; l <= j; ++l) lsum += std::fabs(plan.chol[j * CLTK_MAX_ASSETS + l]);
+          for (uint32_t l = 0; l <= j; ++l) lsum += std::fabs(plan.chol[j * nA + l]);
           const double m = std::fabs(plan.logS0[j]) + std::fabs(st.A[j]) + std::fabs(st.B[j]) * lsum * bw;
           ok = std::isfinite(m) && m < 500.0;
         }
@@ -1345,7 +1345,7 @@ std::string programListing(const CompiledProgram& P) {
   L["kernel_nodes"] = P.kernelNodes;
   L["dag_nodes"] = P.dagNodes;
   Json ch = Json::array();
-  for (uint32_t i = 0; i < CLTK_MAX_ASSETS * CLTK_MAX_ASSETS; ++i) ch.push_back(h.chol[i]);
+  for (uint32_t i = 0; i < nA * nA; ++i) ch.push_back(h.chol[i]);  // rows of n_assets
   L["chol"] = ch;
   Json ls = Json::array();
   for (uint32_t j = 0; j < nA; ++j) ls.push_back(h.logS0[j]);

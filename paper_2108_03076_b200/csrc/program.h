@@ -154,7 +154,7 @@ typedef struct {
   uint32_t log_bounded;     // 1: every path's log-spots provably stay in (-500, 500)
                             // (host bound over the largest normal): the NVRTC payoff's
                             // log-domain ops need no range checks
-  double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, row-major
+  double chol[CLTK_MAX_ASSETS * CLTK_MAX_ASSETS];  // lower factor, rows of n_assets (packed)
   double logS0[CLTK_MAX_ASSETS];                   // log(spot)
 } cltk_plan_header;
 
