@@ -255,7 +255,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
   // jitSource rewrites the header's register window and the steps' classes:
   // JIT_AUTO keeps the interpreter's copy in case NVRTC or the module load fails
   std::vector<cltk_step> interpSteps;
-  std::vector<double> interpInst;  // (jitSource may append reciprocal literal columns)
+  std::vector<double> interpInst, interpShared;  // (jitSource may append reciprocals)
   cltk_plan_header interpHdr{};
   // models of more than CLTK_AOT_MAX_ASSETS assets have no ahead-of-time kernel
   const bool bigModel = I.prog.header.n_assets > CLTK_AOT_MAX_ASSETS;
@@ -270,6 +270,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
     if (use) {
       interpSteps = I.prog.steps;
       interpInst = I.prog.instConst;
+      interpShared = I.prog.sharedConst;
       interpHdr = I.prog.header;
       try {
         jitSrc = jitSource(I.prog);  // assigns steps[].jit_class (uploaded below)
@@ -278,6 +279,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
         jitSrc.clear();
         I.prog.steps = interpSteps;
         I.prog.instConst = interpInst;
+        I.prog.sharedConst = interpShared;
         I.prog.header = interpHdr;
       }
     }
@@ -297,6 +299,7 @@ void Plan::init(const Kernel& k, const void* litsv, const ModelSpec& model,
       I.jitFn = nullptr;
       I.prog.steps = interpSteps;
       I.prog.instConst = interpInst;
+      I.prog.sharedConst = interpShared;
       I.prog.header = interpHdr;
     }
   }

@@ -287,6 +287,12 @@ struct Gen {
   std::set<uint32_t> recipOK;         // instance-literal columns usable as divisors
   uint32_t niCols = 0;                // instance-literal columns before the reciprocals
   mutable std::map<uint32_t, uint32_t> recipCol;     // literal column -> reciprocal column
+  // the same for divisions by shared constants in any block: their
+  // reciprocals are appended to the shared-constant table (JC); not with
+  // copyInst (the instance literals then follow the shared ones in the table)
+  std::set<uint32_t> recipSharedOK;   // shared-constant slots usable as divisors
+  uint32_t ncBase = 0;                // shared constants before the reciprocals
+  mutable std::map<uint32_t, uint32_t> recipShared;  // slot -> reciprocal slot
   mutable std::map<uint32_t, int>* storeRec = nullptr;  // analysis: register -> all stores spot
 
   // Straight-line emission of one block with its values in locals: a register
@@ -397,6 +403,13 @@ struct Gen {
           if (rc == recipCol.end())
             rc = recipCol.emplace(o.b - lit0, niCols + static_cast<uint32_t>(recipCol.size())).first;
           expr = "div_recip(a, b, JI(" + std::to_string(rc->second) + "))";
+        } else if (spotOK && o.op == OP_DIV && sa && o.b >= nThread && o.b < lit0 &&
+                   recipSharedOK.count(o.b - nThread)) {
+          auto rc = recipShared.find(o.b - nThread);
+          if (rc == recipShared.end())
+            rc = recipShared.emplace(o.b - nThread,
+                                     ncBase + static_cast<uint32_t>(recipShared.size())).first;
+          expr = "div_recip(a, b, JC(" + std::to_string(nThread + rc->second) + "))";
         }
         os << ind << "double " << t << ";\n" << ind << "{ const double a = " << a << ";";
         if (!b.empty()) os << " const double b = " << b << ";";
@@ -590,6 +603,14 @@ std::string jitSource(CompiledProgram& prog) {
   // classes is a spot or a log-spot, to a fixed point.
   g.spotOK = g.logMode && h.log_bounded != 0;
   g.niCols = h.n_inst_const;
+  g.ncBase = h.n_shared_const;
+  if (g.spotOK && !g.copyInst) {
+    // shared constants that are safe divisors (the divisions are by R operands)
+    for (uint32_t k = 0; k < h.n_shared_const && k < prog.sharedConst.size(); ++k) {
+      const double v = prog.sharedConst[k];
+      if (std::isfinite(v) && v >= 0x1.0p-100 && v <= 0x1.0p+100) g.recipSharedOK.insert(k);
+    }
+  }
   if (g.spotOK && h.inst_major && h.n_inst_const) {
     for (uint32_t r = h.n_assets; r < h.n_thread; ++r) g.spotRegs.insert(r);
     for (;;) {
@@ -618,8 +639,6 @@ std::string jitSource(CompiledProgram& prog) {
       }
       if (ok) g.recipOK.insert(k);
     }
-  } else {
-    g.spotOK = false;
   }
   std::ostringstream os;
   os << "// Generated by cltk-b200 jit.cpp: payoff policy for one compiled program.\n"
@@ -712,6 +731,12 @@ std::string jitSource(CompiledProgram& prog) {
      << (prog.faultBuild ? "true" : "false")
      << ", " << (h.reg_acc ? 1 : 0) << ", " << (h.stream ? 1 : 0) << ", "
      << (h.inst_major ? 1 : 0) << ">(P, A, accInSmem);\n}\n";
+  // the reciprocal shared constants the steps divide by, RN(1/b) on the host
+  if (!g.recipShared.empty()) {
+    prog.sharedConst.resize(g.ncBase + g.recipShared.size());
+    for (const auto& kv : g.recipShared) prog.sharedConst[kv.second] = 1.0 / prog.sharedConst[kv.first];
+    prog.header.n_shared_const = static_cast<uint32_t>(prog.sharedConst.size());
+  }
   // the reciprocal columns the instance section divides by: RN(1/b) per
   // instance, computed here (IEEE division on the host)
   if (!g.recipCol.empty()) {

@@ -234,6 +234,22 @@ def test_template_batch_divides_by_host_reciprocals():
     assert inst_t.count("div_recip(") == 2 and inst_t.count("__ddiv_rn") == 1
 
 
+def test_step_divisions_by_shared_constants_use_reciprocals():
+    """The worst-off's per-step performance ratios (spot / initial fixing, a
+    shared literal) divide through RN(1/fixing) appended to the shared
+    constants: 15 div_recip per path, no IEEE division left; a fixing out of
+    [2^-100, 2^100] keeps the IEEE division for that operand."""
+    k = load_kernel("worst-off")
+    m = load_model("three")
+    src = E.jit_source(E.Kernel(k), m, [0])
+    assert src.count("div_recip(") == 15 and "__ddiv_rn" not in src
+    base = E.kernel_literals(k)
+    tiny = E.Kernel(k).with_literals({3758.05: 1e-40}) if 3758.05 in base else None
+    if tiny is not None:
+        src = E.jit_source(tiny, m, [0])
+        assert "__ddiv_rn" in src
+
+
 @pytest.mark.gpu
 def test_template_batch_log_domain_minima_bitwise():
     """The same batch priced with the NVRTC kernel (log-domain minima,
