@@ -56,10 +56,10 @@ F_PATH_QMC = {"brc": 102669.7}
 # page, predicated-on DADD + DMUL + 2 DFMA thread instructions,
 # tools/ncu_fp64_flops.py) -- the second roofline figure beside the frozen one.
 NCU_EVIDENCE = {
-    "brc": {"traffic": 201216.0, "fp64_pipe_active": 0.486, "executed_f_path": 173172.4,
-            "capture": "profiles/r2f_path_kernel_brc_10M_{raw.csv,summary.txt} (10M-path launch)"},
-    "worst_off": {"traffic": 70400.0, "fp64_pipe_active": 0.462, "executed_f_path": 2882.4,
-                  "capture": "profiles/r2f_path_kernel_worst_off_4M_{raw.csv,summary.txt}"},
+    "brc": {"traffic": 208384.0, "fp64_pipe_active": 0.486, "executed_f_path": 173142.4,
+            "capture": "profiles/r2h_path_kernel_brc_10M_{raw.csv,summary.txt} (10M-path launch)"},
+    "worst_off": {"traffic": 63232.0, "fp64_pipe_active": 0.470, "executed_f_path": 2732.4,
+                  "capture": "profiles/r2h_path_kernel_worst_off_4M_{raw.csv,summary.txt}"},
     "call": {"traffic": 51200.0, "fp64_pipe_active": 0.429, "executed_f_path": 180.9,
              "capture": "profiles/r2f_path_kernel_call_40M_{raw.csv,summary.txt}"},
 }
