@@ -60,8 +60,8 @@ NCU_EVIDENCE = {
             "capture": "profiles/r2h_path_kernel_brc_10M_{raw.csv,summary.txt} (10M-path launch)"},
     "worst_off": {"traffic": 63232.0, "fp64_pipe_active": 0.470, "executed_f_path": 2732.4,
                   "capture": "profiles/r2h_path_kernel_worst_off_4M_{raw.csv,summary.txt}"},
-    "call": {"traffic": 51200.0, "fp64_pipe_active": 0.429, "executed_f_path": 180.9,
-             "capture": "profiles/r2f_path_kernel_call_40M_{raw.csv,summary.txt}"},
+    "call": {"traffic": 49664.0, "fp64_pipe_active": 0.429, "executed_f_path": 180.9,
+             "capture": "profiles/r2h_path_kernel_call_40M_{raw.csv,summary.txt}"},
 }
 
 BATCH_N = 1024
